@@ -1,0 +1,142 @@
+"""CPU oracle for the JAX-LOB hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` leg may import this package.  The product path
+(``paper_2308_13289_b200``) never imports it and has no CPU fallback.
+
+The arithmetic lives in ``oracle/lob_oracle.c`` (plain C, one book at a time,
+written in the order of PAPER.md Section 4); this module only marshals numpy
+arrays into it.  ``OracleBatch`` mirrors the C ABI of ``include/lob.h`` so that
+parity tests can drive both with the same calls.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "lob_oracle.c")
+_LIB = os.path.join(_HERE, "liblob_oracle.so")
+_lock = threading.Lock()
+_lib = None
+
+NSTATS = 10
+STAT_NAMES = ("msgs", "bad", "trades", "trades_dropped", "traded_qty", "cancelled_qty",
+              "unknown_cancels", "add_overflow", "overflow_qty", "market_discarded_qty")
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (building the checker is not using it)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC",
+                               "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            P = ctypes.c_void_p
+            i32 = ctypes.c_int32
+            lib.oracle_create.restype = P
+            lib.oracle_create.argtypes = [i32, i32, i32, i32, i32]
+            lib.oracle_destroy.argtypes = [P]
+            lib.oracle_init.restype = ctypes.c_int
+            lib.oracle_init.argtypes = [P, i32, i32, P, i32, i32, i32]
+            lib.oracle_process.restype = ctypes.c_int
+            lib.oracle_process.argtypes = [P, i32, i32, P, i32, i32, P]
+            for name in ("oracle_get_book", "oracle_get_l2", "oracle_get_stats",
+                         "oracle_get_violations"):
+                getattr(lib, name).argtypes = [P, P]
+            lib.oracle_get_trades.argtypes = [P, P, P]
+            _lib = lib
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+class OracleBatch:
+    """K independent books of capacity N (SURVEY 8(c) pseudo-code, in C)."""
+
+    def __init__(self, n_books: int, capacity: int, trades_cap: int | None = None,
+                 l2_levels: int = 10, check: bool = False, threads: int = 1):
+        self.lib = _load()
+        self.K, self.N = int(n_books), int(capacity)
+        self.T_cap = self.N if trades_cap is None else int(trades_cap)
+        self.L = int(l2_levels)
+        self.threads = max(1, int(threads))
+        self.ctx = self.lib.oracle_create(self.K, self.N, self.T_cap, self.L, int(bool(check)))
+        if not self.ctx:
+            raise ValueError("oracle_create: bad dimensions")
+        self.init()
+
+    def __del__(self):
+        ctx, self.ctx = getattr(self, "ctx", None), None
+        if ctx:
+            self.lib.oracle_destroy(ctx)
+
+    def _ranges(self):
+        t = min(self.threads, max(1, self.K))
+        step = (self.K + t - 1) // t
+        return [(a, min(self.K, a + step)) for a in range(0, self.K, step)] or [(0, 0)]
+
+    def init(self, init_l2: np.ndarray | None = None, init_ts: int = 0, init_tns: int = 0):
+        L0 = 0
+        if init_l2 is not None:
+            init_l2 = np.ascontiguousarray(init_l2, dtype=np.int32)
+            assert init_l2.ndim == 3 and init_l2.shape[0] == self.K and init_l2.shape[2] == 4
+            L0 = init_l2.shape[1]
+        rc = self.lib.oracle_init(self.ctx, 0, self.K, _ptr(init_l2), L0, int(init_ts), int(init_tns))
+        if rc != 0:
+            raise ValueError("oracle_init: init_levels must be <= capacity")
+
+    def process(self, msgs: np.ndarray, n_steps: int, msgs_per_step: int, l2: bool = True):
+        msgs = np.ascontiguousarray(msgs, dtype=np.int32)
+        assert msgs.shape == (self.K, n_steps * msgs_per_step, 8), msgs.shape
+        out = np.empty((self.K, n_steps, self.L, 4), np.int32) if l2 else None
+        if self.threads == 1 or self.K <= 1:
+            self.lib.oracle_process(self.ctx, 0, self.K, _ptr(msgs), n_steps, msgs_per_step, _ptr(out))
+        else:
+            with ThreadPoolExecutor(self.threads) as ex:   # ctypes releases the GIL
+                list(ex.map(lambda r: self.lib.oracle_process(
+                    self.ctx, r[0], r[1], _ptr(msgs), n_steps, msgs_per_step, _ptr(out)),
+                    self._ranges()))
+        return out
+
+    def book(self) -> np.ndarray:
+        out = np.empty((self.K, 2, self.N, 6), np.int32)
+        self.lib.oracle_get_book(self.ctx, _ptr(out))
+        return out
+
+    def trades(self):
+        out = np.empty((self.K, self.T_cap, 6), np.int32)
+        cnt = np.empty((self.K,), np.int32)
+        self.lib.oracle_get_trades(self.ctx, _ptr(out), _ptr(cnt))
+        return out, cnt
+
+    def l2(self) -> np.ndarray:
+        out = np.empty((self.K, self.L, 4), np.int32)
+        self.lib.oracle_get_l2(self.ctx, _ptr(out))
+        return out
+
+    def stats(self) -> np.ndarray:
+        out = np.empty((self.K, NSTATS), np.int64)
+        self.lib.oracle_get_stats(self.ctx, _ptr(out))
+        return out
+
+    def violations(self) -> np.ndarray:
+        out = np.empty((self.K,), np.int64)
+        self.lib.oracle_get_violations(self.ctx, _ptr(out))
+        return out
