@@ -1,0 +1,32 @@
+# Builds every native artefact in-tree (the .so files travel to the GPU box with gpurun).
+#   paper_2308_13289_b200/liblob.so   CUDA engine behind include/lob.h (sm_100a only)
+#   oracle/liblob_oracle.so           CPU oracle (test infrastructure)
+#   lobgen/liblobgen.so               seeded input generator
+NVCC      ?= /usr/local/cuda/bin/nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xptxas -v -Xcompiler -fPIC,-O2 -shared
+PKG       := paper_2308_13289_b200
+LIB       := $(PKG)/liblob.so
+SRCS      := $(PKG)/csrc/lob_api.cu
+DEPS      := $(SRCS) $(PKG)/csrc/lob_kernels.cuh include/lob.h
+
+all: $(LIB) oracle/liblob_oracle.so lobgen/liblobgen.so
+
+$(LIB): $(DEPS)
+	$(NVCC) $(NVFLAGS) -o $@.tmp $(SRCS) 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; exit 1)
+	mv $@.tmp $@
+	@grep -E "Compiling entry|registers|spill" $(PKG)/ptxas.log | grep -B1 -E "spill stores [1-9]|bytes spill" || true
+
+oracle/liblob_oracle.so: oracle/lob_oracle.c
+	gcc -O2 -std=c11 -Wall -shared -fPIC -o $@ $<
+
+lobgen/liblobgen.so: lobgen/lobgen.c
+	gcc -O2 -std=c11 -Wall -shared -fPIC -pthread -o $@ $<
+
+sass: $(LIB)
+	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > $(PKG)/liblob.sass
+
+clean:
+	rm -f $(LIB) oracle/liblob_oracle.so lobgen/liblobgen.so $(PKG)/ptxas.log $(PKG)/liblob.sass
+
+.PHONY: all clean sass

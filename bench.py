@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark of the batched LOB hot path (BASELINE.json metric: whole-box messages/s,
+ns/message and HBM-roofline fraction at 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+A *step* is one pass of the whole hot path over one batch: lob_init (a0: empty
+books + synthetic L2 seed) followed by lob_process_messages over every book's
+1,000-message stream (a1-a11, L2 top-10 after each of the 10 steps of 100).
+Inputs are resident in HBM before the timed region; the messages (2.1 GB per GPU
+for C4) exceed the 126 MB L2, so no flush is needed between steps.
+
+Multi-GPU (torchrun, one process per GPU): every rank owns its own 65,536 books
+(global ids rank*K..), so per-GPU work is fixed ("weak" scaling); there is no
+communication on the hot path; NCCL only gathers per-book counters and the max
+elapsed time afterwards.
+
+--impl reference times the CPU oracle (the reference arm for this tier) on the
+host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import lobgen  # noqa: E402
+
+LOGICAL_ORDER_BYTES = 24   # Eq.2: 6 x int32
+MSG_BYTES = 32             # Eq.6: 8 x int32
+TRADE_BYTES = 24           # Eq.3: 6 x int32
+L2_LEVEL_BYTES = 16        # [ask_p, ask_q, bid_p, bid_q]
+STAT_BYTES = 80            # 10 x int64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", float(d.get("sm_max_mhz", 1965.0))
+    return 6650.0, "fallback (B200_PROFILING.md)", 1965.0
+
+
+def workload_desc(cfg, K):
+    return (f"{cfg.name}: {K} books/GPU x capacity {cfg.capacity}, {cfg.n_msgs} {cfg.profile} messages/book "
+            f"({cfg.n_steps} steps x {cfg.msgs_per_step}), L2 top-{cfg.l2_levels} per step, "
+            f"init L2 seed {cfg.init_levels} levels/side")
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as exc:  # pragma: no cover - no NVML
+            self.err = str(exc)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = lobgen.CONFIGS[args.config]
+    cores = len(os.sched_getaffinity(0))
+    nb = 2048  # bounded sample per step
+    msgs, init = lobgen.generate(cfg, n_books=nb)
+    o = oracle.OracleBatch(nb, cfg.capacity, cfg.trades_cap, cfg.l2_levels, threads=cores)
+
+    def step():
+        o.init(init, lobgen.INIT_TS, lobgen.INIT_TNS)
+        o.process(msgs, cfg.n_steps, cfg.msgs_per_step)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    n = nb * cfg.n_msgs * args.steps
+    v = n / dt
+    sample = f"first {nb} books of {cfg.name} ({nb * cfg.n_msgs} messages) per step, {args.steps} steps"
+    line = {"impl": "reference", "metric": "messages/sec", "value": v, "unit": "msg/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic", "ns_per_message": 1e9 / v,
+            "config": {"workload": workload_desc(cfg, nb), "books": nb, "capacity": cfg.capacity},
+            "cpu_baseline": {"value": v, "unit": "msg/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "msg/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- CPU baseline leg
+def cpu_baseline(cfg, msgs_h, init_h, seconds, gpu_stats_h):
+    """The oracle as it stands, on the host cores, over a bounded sample of the same
+    workload (leading books, growing until ~`seconds` of CPU time)."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    nb, done_books, total = 512, 0, 0.0
+    match = True
+    while total < seconds and done_books < cfg.n_books:
+        n = min(nb, cfg.n_books - done_books)
+        sl = slice(done_books, done_books + n)
+        o = oracle.OracleBatch(n, cfg.capacity, cfg.trades_cap, cfg.l2_levels, threads=cores)
+        m = np.ascontiguousarray(msgs_h[sl])
+        i = np.ascontiguousarray(init_h[sl])
+        t0 = time.perf_counter()
+        o.init(i, lobgen.INIT_TS, lobgen.INIT_TNS)
+        o.process(m, cfg.n_steps, cfg.msgs_per_step)
+        total += time.perf_counter() - t0
+        match = match and np.array_equal(o.stats(), gpu_stats_h[sl])
+        done_books += n
+        nb *= 2
+    v = done_books * cfg.n_msgs / total
+    return {"value": v, "unit": "msg/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {done_books} of {cfg.n_books} books of {cfg.name} "
+                      f"({done_books * cfg.n_msgs} messages, {total:.1f} s wall on {cores} threads over books)",
+            "counters_match_gpu": bool(match)}
+
+
+# ------------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch.distributed as dist
+
+    from paper_2308_13289_b200 import LobBatch, launch_count
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = lobgen.CONFIGS[args.config]
+    K = cfg.n_books
+    S, M, L = cfg.n_steps, cfg.msgs_per_step, cfg.l2_levels
+
+    # inputs: generated on the host (seeded by GLOBAL book id), pinned, then resident in HBM
+    msgs_h = torch.empty((K, cfg.n_msgs, 8), dtype=torch.int32).pin_memory()
+    init_h = torch.empty((K, cfg.init_levels, 4), dtype=torch.int32).pin_memory()
+    t0 = time.time()
+    lobgen.generate(cfg, book_begin=rank * K, msgs_out=msgs_h.numpy(), init_out=init_h.numpy())
+    gen_s = time.time() - t0
+    msgs_d = msgs_h.to(dev)
+    init_d = init_h.to(dev)
+    l2_d = torch.empty((K, S, L, 4), dtype=torch.int32, device=dev)
+    b = LobBatch(K, cfg.capacity, cfg.trades_cap, L, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        b.init(init_d, lobgen.INIT_TS, lobgen.INIT_TNS)
+        if evs is not None:
+            evs[0].record(stream)
+        b.process(msgs_d, S, M, l2_out=l2_d)
+        if evs is not None:
+            evs[1].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    n_launch0 = launch_count()
+    torch.cuda.synchronize()
+    with sampler:
+        start.record(stream)
+        for i in range(args.steps):
+            step(kev[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    n_launch = launch_count() - n_launch0
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = start.elapsed_time(end)
+    kernel_ms = [a.elapsed_time(z) for a, z in kev]
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+
+    # per-book counters and the trade counts of the last step (algorithmic bytes)
+    st = b.stats()
+    _, ntr = b.trades()
+    trades_logged = int(ntr.sum().item())
+    if world > 1:
+        allst = torch.empty((world * K, st.shape[1]), dtype=st.dtype, device=dev)
+        dist.all_gather_into_tensor(allst, st)
+        tot = torch.tensor([trades_logged], dtype=torch.int64, device=dev)
+        dist.all_reduce(tot)
+        trades_total = int(tot.item())
+    else:
+        allst = st
+        trades_total = trades_logged
+    stats_sum = allst.sum(0).cpu().tolist()
+
+    total_msgs = world * K * cfg.n_msgs * args.steps
+    value = total_msgs / (elapsed_ms / 1e3)
+    ms_per_step = elapsed_ms / args.steps
+
+    # roofline of the dominant kernel (lob_step): algorithmic bytes per launch
+    book_bytes = 2 * K * 2 * cfg.capacity * LOGICAL_ORDER_BYTES     # state read + written once
+    alg_bytes = (K * cfg.n_msgs * MSG_BYTES + trades_logged * TRADE_BYTES + K * S * L * L2_LEVEL_BYTES
+                 + book_bytes + 2 * K * STAT_BYTES)
+    kmean_ms = statistics.mean(kernel_ms)
+    peak, peak_src, _ = load_peaks()
+    achieved = alg_bytes / (kmean_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "lob_step_reg<4,4> (lob_process_messages)",
+                "kernel_ms": kmean_ms, "kernel_share_of_step": kmean_ms / ms_per_step,
+                "alg_bytes_per_launch": alg_bytes, "alg_bytes_per_msg": alg_bytes / (K * cfg.n_msgs),
+                "peak_source": peak_src}
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            tr = json.load(open(prof)).get(cfg.name)
+            if tr:
+                roofline["traffic"] = tr["dram_bytes_per_launch"]
+                roofline["traffic_source"] = tr["source"]
+        except Exception:
+            pass
+
+    # end-to-end through the public API with HOST buffers: pinned H2D of the step's
+    # messages and L2 seed, processing, D2H of the L2 snapshots and counters
+    e2e = None
+    if args.e2e_steps > 0:
+        h_l2 = torch.empty((K, S, L, 4), dtype=torch.int32).pin_memory()
+        h_st = torch.empty((K, 10), dtype=torch.int64).pin_memory()
+        e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def e2e_step():
+            init_d.copy_(init_h, non_blocking=True)
+            b.init(init_d, lobgen.INIT_TS, lobgen.INIT_TNS)
+            b.process_host(msgs_h, S, M, h_l2, h_st, msgs_d, l2_d, chunks=8)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e_s.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e_e.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e_s.elapsed_time(e_e)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_v = world * K * cfg.n_msgs * args.e2e_steps / (float(et.item()) / 1e3)
+        e2e = {"value": e2e_v, "unit": "msg/s",
+               "h2d_bytes_per_step": msgs_h.numel() * 4 + init_h.numel() * 4,
+               "d2h_bytes_per_step": h_l2.numel() * 4 + h_st.numel() * 8,
+               "path": "LobBatch.process_host -> lob_process_messages_host (8 pipelined chunks)"}
+        assert torch.equal(h_st, st.cpu()), "end-to-end counters differ from the device run"
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, msgs_h.numpy(), init_h.numpy(), args.cpu_seconds, st.cpu().numpy())
+
+    if rank == 0:
+        line = {"metric": "messages/sec", "value": value, "unit": "msg/s", "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                "ns_per_message": 1e9 / value, "ns_per_message_per_gpu": 1e9 / value * world,
+                "config": {"workload": workload_desc(cfg, K), "books_per_gpu": K, "books_total": world * K,
+                           "capacity": cfg.capacity, "msgs_per_book": cfg.n_msgs, "n_steps": S,
+                           "msgs_per_step": M, "l2_levels": L, "trades_cap": cfg.trades_cap,
+                           "profile": cfg.profile, "seed": cfg.seed, "parallelism": f"books sharded x{world}",
+                           "l2_flush": "inputs larger than L2 (messages %.2f GB/GPU > 126 MB)"
+                                       % (msgs_h.numel() * 4 / 1e9)},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": n_launch,
+                "clocks": sampler.summary(),
+                "totals": dict(zip(["msgs", "bad", "trades", "trades_dropped", "traded_qty", "cancelled_qty",
+                                    "unknown_cancels", "add_overflow", "overflow_qty", "market_discarded_qty"],
+                                   stats_sum)),
+                "trades_logged_last_step": trades_total, "generate_s": gen_s}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

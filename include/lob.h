@@ -1,0 +1,143 @@
+/*
+ * include/lob.h -- C ABI of the B200 batched limit-order-book engine.
+ *
+ * The engine runs the data-parallel hot path of JAX-LOB (arXiv 2308.13289,
+ * PAPER.md Section 4): K independent books, each two fixed-capacity unsorted
+ * order arrays, step through message streams; every message is an add, a
+ * cancel/delete or a match with trade logging; an L2 snapshot is taken after
+ * every step.  Citations "P:Lnnn" are lines of PAPER.md; "Gnn" are the
+ * readings listed in DESIGN.md (ambiguity ledger).
+ *
+ * Conventions (all entry points):
+ *  - Memory: every device buffer is allocated by the CALLER (e.g. torch CUDA
+ *    tensors) and passed as a raw pointer; the library never allocates or
+ *    frees device memory.  The state buffer (lob_state_bytes) must outlive the
+ *    context and be 256-byte aligned.
+ *  - Streams: every call enqueues asynchronously on the given cudaStream_t
+ *    (pass torch's current stream; NULL = legacy default stream); nothing
+ *    synchronises implicitly except lob_process_messages_host, which does not
+ *    synchronise either (the caller waits on the stream).
+ *  - Errors: return codes report caller mistakes only (bad dimensions, NULL
+ *    required pointer, wrong device, size overflow, unsupported capacity) and
+ *    CUDA launch failures (LOB_ECUDA, detail in lob_last_error()).
+ *    Data-dependent conditions are never errors: they are per-book counters
+ *    (add overflow, trade-log overflow, unknown cancel, malformed message).
+ *  - Threads: a context is used by one host thread at a time; one context per
+ *    device and process.
+ *  - Layouts: all records are int32 in the paper's field order; counters int64.
+ */
+#ifndef LOB_H
+#define LOB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOB_MSG_FIELDS 8    /* Eq.6  m = [T, S, Q, P, OID, TID, Ts, Tns] */
+#define LOB_ORDER_FIELDS 6  /* Eq.2  o = [P, Q, OID, TID, Ts, Tns] */
+#define LOB_TRADE_FIELDS 6  /* Eq.3  t = [P, Q, OID_aggr, OID_stand, Ts, Tns] P:L187 */
+#define LOB_L2_FIELDS 4     /* [ask_p, ask_q, bid_p, bid_q] per level (G23)           */
+#define LOB_MAX_CAPACITY 2048
+#define LOB_MAX_L2_LEVELS 32
+
+enum { LOB_LIMIT = 1, LOB_CANCEL = 2, LOB_DELETE = 3, LOB_MARKET = 4 };
+enum { LOB_BID = 1, LOB_ASK = -1 };
+enum { LOB_OK = 0, LOB_EINVAL = -1, LOB_ECUDA = -2, LOB_ENOMEM = -3, LOB_EUNSUPPORTED = -4 };
+
+/* per-book counters, cumulative since lob_init */
+enum {
+    LOB_ST_MSGS = 0,             /* every message, including padding (T=0) and malformed   */
+    LOB_ST_BAD,                  /* malformed: T not in 1..4, S not +-1, limit P<=0,
+                                    cancel/delete Q<=0 (G22)                                */
+    LOB_ST_TRADES,               /* fills executed (logged or not)                          */
+    LOB_ST_TRADES_DROPPED,       /* fills whose record did not fit the trade log (G8)       */
+    LOB_ST_TRADED_QTY,           /* sum of fill quantities                                  */
+    LOB_ST_CANCELLED_QTY,        /* sum of min(Q_cancel, Q_resting) (G14)                   */
+    LOB_ST_UNKNOWN_CANCELS,      /* cancels/deletes that found no order (G15)               */
+    LOB_ST_ADD_OVERFLOW,         /* limit remainders dropped because the side was full (G6) */
+    LOB_ST_OVERFLOW_QTY,         /* their quantity                                          */
+    LOB_ST_MARKET_DISCARDED_QTY, /* unmatched market quantity, disregarded         */
+    LOB_NSTATS
+};
+
+typedef struct {
+    int32_t n_books;    /* K >= 0: independent books                          */
+    int32_t capacity;   /* N in 1..LOB_MAX_CAPACITY: orders per side (Eq.1)    */
+    int32_t trades_cap; /* rows of the trade log per book per call (Eq.4, G7), >= 0    */
+    int32_t l2_levels;  /* L in 1..LOB_MAX_L2_LEVELS: levels per L2 snapshot (G23)     */
+    int32_t device;     /* CUDA device ordinal the state lives on (must be current)    */
+} lob_config;
+
+typedef struct lob_ctx lob_ctx; /* opaque host-side handle: dims, pointers, launch config */
+
+/* Bytes of device state for `cfg` (books in an internal padded SoA layout, the
+ * trade logs, trade counts and counters).  0 if cfg is invalid. */
+size_t lob_state_bytes(const lob_config *cfg);
+
+/* Create a host handle over caller-allocated device state (no GPU work).
+ * Returns LOB_EINVAL for a bad config / NULL / misaligned state,
+ * LOB_EUNSUPPORTED for capacity > LOB_MAX_CAPACITY, LOB_ECUDA if the device
+ * cannot be queried. */
+int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state);
+void lob_destroy(lob_ctx *ctx); /* frees the host handle only */
+
+/* a0: book init.  Both sides and the trade log become -1
+ * (P:L168), counters zero.  If d_init_l2 is non-NULL it is a
+ * [K][init_levels][4] int32 Level-2 snapshot [ask_p, ask_q, bid_p, bid_q] per
+ * level: one synthetic order per populated level (P>0 and Q>0, G24),
+ * OIDs -9000, -9001, ... over asks best->worst then bids, TID -9000, time
+ * (init_ts, init_tns).  init_levels must be <= capacity. */
+int lob_init(lob_ctx *ctx, const int32_t *d_init_l2, int32_t init_levels, int32_t init_ts,
+             int32_t init_tns, void *cuda_stream);
+
+/* a1..a11: process n_steps*msgs_per_step messages per book.
+ *  d_msgs:   [K][n_steps*msgs_per_step][8] int32, Eq.6 order (G19); book k's
+ *            stream is processed serially in order, books in parallel.
+ *            Message rules: P:L287-292; T=0 is padding (G21).
+ *  d_l2_out: NULL or [K][n_steps][L][4] int32, the L2 snapshot after the last
+ *            message of every step (absent levels (-1, 0), G23).
+ * The trade log is cleared at the start of the call (G9); counters accumulate.
+ * n_steps*msgs_per_step == 0 is allowed (clears the trade log only). */
+int lob_process_messages(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps,
+                         int32_t msgs_per_step, int32_t *d_l2_out, void *cuda_stream);
+
+/* Same call with HOST buffers (end-to-end path): copies h_msgs (pinned host,
+ * [K][n_steps*msgs_per_step][8]) into the caller's device buffer d_msgs_buf,
+ * processes it, and copies the L2 snapshots (if h_l2_out is non-NULL; device
+ * staging in d_l2_buf, [K][n_steps][L][4]) and the counters (if h_stats_out is
+ * non-NULL, [K][LOB_NSTATS] int64, staged in the state) back to the host.
+ * Books are processed in `chunks` slices so that copies overlap kernels; all
+ * work is enqueued on cuda_stream plus one internal event chain, and the
+ * caller synchronises the stream before reading host outputs. */
+int lob_process_messages_host(lob_ctx *ctx, const int32_t *h_msgs, int32_t n_steps,
+                              int32_t msgs_per_step, int32_t *h_l2_out, int64_t *h_stats_out,
+                              int32_t *d_msgs_buf, int32_t *d_l2_buf, int32_t chunks,
+                              void *cuda_stream);
+
+/* Current L2 snapshot of every book: d_out [K][L][4] int32. */
+int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *cuda_stream);
+
+/* Trade log of the last call: d_out [K][trades_cap][6] int32 (rows >=
+ * count are -1), d_counts [K] int32 (nullable). */
+int lob_get_trades(lob_ctx *ctx, int32_t *d_out, int32_t *d_counts, void *cuda_stream);
+
+/* Full book state for parity/checkpointing: d_out [K][2][N][6] int32,
+ * side 0 = asks (A), side 1 = bids (B); empty slots all -1. */
+int lob_get_book(lob_ctx *ctx, int32_t *d_out, void *cuda_stream);
+
+/* Counters: d_out [K][LOB_NSTATS] int64. */
+int lob_get_stats(lob_ctx *ctx, int64_t *d_out, void *cuda_stream);
+
+/* Number of kernels this process has launched through the library (all contexts). */
+int64_t lob_launch_count(void);
+
+const char *lob_strerror(int code);
+const char *lob_last_error(void); /* thread-local detail for the last failure */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOB_H */

@@ -1,0 +1,358 @@
+// lob_api.cu -- host shim of the C ABI declared in include/lob.h.
+// Validation, state layout, launch configuration; all compute is in
+// lob_kernels.cuh.  No CPU fallback: every entry point either launches the
+// sm_100a kernels or returns an error.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/lob.h"
+#include "lob_kernels.cuh"
+
+using namespace lobk;
+
+static_assert((int)NST == (int)LOB_NSTATS, "counter layout");
+static_assert(F_P == 0 && F_TNS == 5, "field order");
+
+namespace {
+thread_local char g_err[512] = "";
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const char *fmt, const char *detail = "") {
+    snprintf(g_err, sizeof(g_err), fmt, detail);
+    return code;
+}
+int cuda_fail(cudaError_t e, const char *where) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return LOB_ECUDA;
+}
+
+constexpr int REG_WARPS = 4;  // warps (books) per CTA on the register path
+
+// slots per lane: 1..4 registers, 8/16/32/64 shared memory
+int kpl_bucket(int N) {
+    int k = (N + 31) / 32;
+    if (k <= 4) return k;
+    int b = 8;
+    while (b < k) b <<= 1;
+    return b;
+}
+
+struct Layout {
+    int NP;
+    size_t off_book, off_trades, off_ntr, off_stats, total;
+};
+
+bool layout_of(const lob_config *c, Layout *L) {
+    if (!c || c->n_books < 0 || c->capacity < 1 || c->capacity > LOB_MAX_CAPACITY || c->trades_cap < 0 ||
+        c->l2_levels < 1 || c->l2_levels > LOB_MAX_L2_LEVELS)
+        return false;
+    const size_t K = (size_t)c->n_books;
+    L->NP = 32 * kpl_bucket(c->capacity);
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    L->off_book = 0;
+    L->off_trades = al(L->off_book + K * 2 * NF * L->NP * sizeof(int32_t));
+    L->off_ntr = al(L->off_trades + K * (size_t)c->trades_cap * 6 * sizeof(int32_t));
+    L->off_stats = al(L->off_ntr + K * sizeof(int32_t));
+    L->total = al(L->off_stats + K * NST * sizeof(long long));
+    return true;
+}
+}  // namespace
+
+struct lob_ctx {
+    lob_config cfg;
+    Layout lay;
+    char *state;
+    int sm_count;
+    int kpl;
+    int grid_cap;  // persistent grid: resident CTAs for the step kernel
+    size_t smem_bytes;
+    int32_t *book() const { return reinterpret_cast<int32_t *>(state + lay.off_book); }
+    int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
+    int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
+    long long *stats() const { return reinterpret_cast<long long *>(state + lay.off_stats); }
+};
+
+namespace {
+template <class F>
+void for_kpl(int kpl, F &&f) {
+    switch (kpl) {
+        case 1: f(std::integral_constant<int, 1>()); break;
+        case 2: f(std::integral_constant<int, 2>()); break;
+        case 3: f(std::integral_constant<int, 3>()); break;
+        case 4: f(std::integral_constant<int, 4>()); break;
+        case 8: f(std::integral_constant<int, 8>()); break;
+        case 16: f(std::integral_constant<int, 16>()); break;
+        case 32: f(std::integral_constant<int, 32>()); break;
+        default: f(std::integral_constant<int, 64>()); break;
+    }
+}
+
+int check_ctx(lob_ctx *ctx) {
+    if (!ctx) return fail(LOB_EINVAL, "null context%s");
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev != ctx->cfg.device) return fail(LOB_EINVAL, "context device is not the current device%s");
+    return LOB_OK;
+}
+
+int after_launch(const char *what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? LOB_OK : cuda_fail(e, what);
+}
+
+unsigned blocks_for(long long threads, int bs) { return (unsigned)((threads + bs - 1) / bs); }
+
+int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M, int32_t *d_l2, int book0, int nb,
+                cudaStream_t st) {
+    if (nb <= 0) return LOB_OK;
+    Params p;
+    p.book = ctx->book(); p.trades = ctx->trades(); p.ntrades = ctx->ntr(); p.stats = ctx->stats();
+    p.msgs = d_msgs; p.l2out = d_l2;
+    p.N = ctx->cfg.capacity; p.NP = ctx->lay.NP; p.Tcap = ctx->cfg.trades_cap; p.L = ctx->cfg.l2_levels;
+    p.n_steps = n_steps; p.M = M; p.book0 = book0; p.nb = nb;
+    int rc = LOB_OK;
+    for_kpl(ctx->kpl, [&](auto kc) {
+        constexpr int KPL = decltype(kc)::value;
+        if constexpr (KPL <= 4) {
+            const unsigned need = blocks_for(nb, REG_WARPS);
+            const unsigned grid = need < (unsigned)ctx->grid_cap ? need : (unsigned)ctx->grid_cap;
+            lob_step_reg<KPL, REG_WARPS><<<grid, REG_WARPS * 32, 0, st>>>(p);
+        } else {
+            const unsigned grid = (unsigned)nb < (unsigned)ctx->grid_cap ? (unsigned)nb : (unsigned)ctx->grid_cap;
+            lob_step_smem<KPL><<<grid, 32, ctx->smem_bytes, st>>>(p);
+        }
+        rc = after_launch("lob_step kernel");
+    });
+    return rc;
+}
+}  // namespace
+
+extern "C" {
+
+size_t lob_state_bytes(const lob_config *cfg) {
+    Layout L;
+    return layout_of(cfg, &L) ? L.total : 0;
+}
+
+int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
+    if (!out) return fail(LOB_EINVAL, "out is null%s");
+    *out = nullptr;
+    if (cfg && cfg->capacity > LOB_MAX_CAPACITY) return fail(LOB_EUNSUPPORTED, "capacity > LOB_MAX_CAPACITY%s");
+    Layout L;
+    if (!layout_of(cfg, &L)) return fail(LOB_EINVAL, "invalid lob_config%s");
+    if (!d_state && cfg->n_books > 0) return fail(LOB_EINVAL, "state is null%s");
+    if (reinterpret_cast<uintptr_t>(d_state) % 256) return fail(LOB_EINVAL, "state must be 256-byte aligned%s");
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev != cfg->device) return fail(LOB_EINVAL, "cfg.device is not the current device%s");
+    int sms = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    lob_ctx *c = new (std::nothrow) lob_ctx();
+    if (!c) return fail(LOB_ENOMEM, "host allocation failed%s");
+    c->cfg = *cfg;
+    c->lay = L;
+    c->state = static_cast<char *>(d_state);
+    c->sm_count = sms;
+    c->kpl = kpl_bucket(cfg->capacity);
+    int per_sm = 1;
+    int rc = LOB_OK;
+    for_kpl(c->kpl, [&](auto kc) {
+        constexpr int KPL = decltype(kc)::value;
+        if constexpr (KPL <= 4) {
+            c->smem_bytes = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step_reg<KPL, REG_WARPS>, REG_WARPS * 32, 0);
+        } else {
+            c->smem_bytes = (2 * CH * 8 + 8) * sizeof(int32_t) + (size_t)2 * NF * KPL * 32 * sizeof(int32_t);
+            e = cudaFuncSetAttribute(lob_step_smem<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)c->smem_bytes);
+            if (e == cudaSuccess)
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step_smem<KPL>, 32, c->smem_bytes);
+        }
+        if (e != cudaSuccess) rc = cuda_fail(e, "occupancy query");
+    });
+    if (rc != LOB_OK) { delete c; return rc; }
+    c->grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    *out = c;
+    return LOB_OK;
+}
+
+void lob_destroy(lob_ctx *ctx) { delete ctx; }
+
+int lob_init(lob_ctx *ctx, const int32_t *d_init_l2, int32_t init_levels, int32_t init_ts, int32_t init_tns,
+             void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (init_levels < 0 || init_levels > ctx->cfg.capacity) return fail(LOB_EINVAL, "init_levels must be in 0..capacity%s");
+    if (d_init_l2 && init_levels == 0) d_init_l2 = nullptr;
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    const int wpb = 8;
+    lob_init_kernel<<<blocks_for(K, wpb), wpb * 32, 0, (cudaStream_t)stream>>>(
+        ctx->book(), ctx->trades(), ctx->ntr(), ctx->stats(), K, ctx->cfg.capacity, ctx->lay.NP, ctx->cfg.trades_cap,
+        d_init_l2, init_levels, init_ts, init_tns);
+    return after_launch("lob_init_kernel");
+}
+
+int lob_process_messages(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t msgs_per_step,
+                         int32_t *d_l2_out, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (n_steps < 0 || msgs_per_step < 0) return fail(LOB_EINVAL, "negative n_steps/msgs_per_step%s");
+    const long long nmsg = (long long)n_steps * msgs_per_step;
+    if (nmsg > (1ll << 30)) return fail(LOB_EINVAL, "n_steps*msgs_per_step overflows%s");
+    if (nmsg > 0 && !d_msgs && ctx->cfg.n_books > 0) return fail(LOB_EINVAL, "d_msgs is null%s");
+    if (reinterpret_cast<uintptr_t>(d_msgs) % 16) return fail(LOB_EINVAL, "d_msgs must be 16-byte aligned%s");
+    if (reinterpret_cast<uintptr_t>(d_l2_out) % 16) return fail(LOB_EINVAL, "d_l2_out must be 16-byte aligned%s");
+    if (msgs_per_step == 0) n_steps = 0;
+    return launch_step(ctx, d_msgs, n_steps, msgs_per_step, n_steps > 0 ? d_l2_out : nullptr, 0, ctx->cfg.n_books,
+                       (cudaStream_t)stream);
+}
+
+int lob_process_messages_host(lob_ctx *ctx, const int32_t *h_msgs, int32_t n_steps, int32_t msgs_per_step,
+                              int32_t *h_l2_out, int64_t *h_stats_out, int32_t *d_msgs_buf, int32_t *d_l2_buf,
+                              int32_t chunks, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (n_steps < 0 || msgs_per_step < 0 || chunks < 1) return fail(LOB_EINVAL, "bad n_steps/msgs_per_step/chunks%s");
+    const long long nmsg = (long long)n_steps * msgs_per_step;
+    if (nmsg > (1ll << 30)) return fail(LOB_EINVAL, "n_steps*msgs_per_step overflows%s");
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    if ((nmsg > 0 && (!h_msgs || !d_msgs_buf)) || (h_l2_out && !d_l2_buf))
+        return fail(LOB_EINVAL, "null buffer%s");
+    if (msgs_per_step == 0) n_steps = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int L = ctx->cfg.l2_levels;
+    const size_t msg_bytes_pb = (size_t)nmsg * 8 * sizeof(int32_t);
+    const size_t l2_bytes_pb = (size_t)n_steps * L * 4 * sizeof(int32_t);
+    const int per = (K + chunks - 1) / chunks;
+    // Three-stage pipeline over book chunks: H2D(i) on `h2d`, kernel(i) on the
+    // caller's stream after H2D(i), D2H(i) on `d2h` after kernel(i); copies of
+    // neighbouring chunks overlap the kernels on the two copy engines.
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    cudaEvent_t start, done_h, done_k;
+    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done_h, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done_k, cudaEventDisableTiming);
+    cudaEventRecord(start, st);
+    cudaStreamWaitEvent(h2d, start, 0);
+    cudaStreamWaitEvent(d2h, start, 0);
+    for (int i = 0; i < chunks && rc == LOB_OK; ++i) {
+        const int b0 = i * per, nb = (b0 + per <= K) ? per : K - b0;
+        if (nb <= 0) break;
+        if (msg_bytes_pb) {
+            e = cudaMemcpyAsync((char *)d_msgs_buf + (size_t)b0 * msg_bytes_pb,
+                                (const char *)h_msgs + (size_t)b0 * msg_bytes_pb, (size_t)nb * msg_bytes_pb,
+                                cudaMemcpyHostToDevice, h2d);
+            if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
+        }
+        cudaEventRecord(done_h, h2d);          // events may be re-recorded: waits capture the
+        cudaStreamWaitEvent(st, done_h, 0);    // state at the time of the wait call
+        rc = launch_step(ctx, d_msgs_buf + (size_t)b0 * nmsg * 8, n_steps, msgs_per_step,
+                         (h_l2_out && n_steps) ? d_l2_buf + (size_t)b0 * n_steps * L * 4 : nullptr, b0, nb, st);
+        if (rc) break;
+        if (h_l2_out && l2_bytes_pb) {
+            cudaEventRecord(done_k, st);
+            cudaStreamWaitEvent(d2h, done_k, 0);
+            e = cudaMemcpyAsync((char *)h_l2_out + (size_t)b0 * l2_bytes_pb,
+                                (char *)d_l2_buf + (size_t)b0 * l2_bytes_pb, (size_t)nb * l2_bytes_pb,
+                                cudaMemcpyDeviceToHost, d2h);
+            if (e != cudaSuccess) { rc = cuda_fail(e, "D2H"); break; }
+        }
+    }
+    cudaEventRecord(done_h, d2h);              // the caller's stream completes after every D2H
+    cudaStreamWaitEvent(st, done_h, 0);
+    if (rc == LOB_OK && h_stats_out) {
+        e = cudaMemcpyAsync(h_stats_out, ctx->stats(), (size_t)K * NST * sizeof(long long), cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "D2H stats");
+    }
+    // resources are released once the enqueued work no longer needs them
+    cudaEventDestroy(start);
+    cudaEventDestroy(done_h);
+    cudaEventDestroy(done_k);
+    cudaStreamDestroy(h2d);
+    cudaStreamDestroy(d2h);
+    return rc;
+}
+
+int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    if (!d_out || reinterpret_cast<uintptr_t>(d_out) % 16) return fail(LOB_EINVAL, "d_out null or misaligned%s");
+    for_kpl(ctx->kpl, [&](auto kc) {
+        constexpr int KPL = decltype(kc)::value;
+        if constexpr (KPL <= 4)
+            lob_export_l2_reg<KPL><<<blocks_for(K, 4), 128, 0, (cudaStream_t)stream>>>(
+                ctx->book(), d_out, K, ctx->cfg.capacity, ctx->lay.NP, ctx->cfg.l2_levels);
+        else
+            lob_export_l2_smem<KPL><<<K, 32, 0, (cudaStream_t)stream>>>(ctx->book(), d_out, K, ctx->cfg.capacity,
+                                                                          ctx->lay.NP, ctx->cfg.l2_levels);
+        rc = after_launch("lob_export_l2");
+    });
+    return rc;
+}
+
+int lob_get_trades(lob_ctx *ctx, int32_t *d_out, int32_t *d_counts, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    if (!d_out && ctx->cfg.trades_cap > 0) return fail(LOB_EINVAL, "d_out is null%s");
+    const long long n = (long long)K * ctx->cfg.trades_cap * 6;
+    const long long threads = n > K ? n : K;
+    lob_export_trades<<<blocks_for(threads, 256), 256, 0, (cudaStream_t)stream>>>(ctx->trades(), ctx->ntr(), d_out,
+                                                                                   d_counts, K, ctx->cfg.trades_cap);
+    return after_launch("lob_export_trades");
+}
+
+int lob_get_book(lob_ctx *ctx, int32_t *d_out, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    if (!d_out) return fail(LOB_EINVAL, "d_out is null%s");
+    lob_export_book<<<blocks_for((long long)K * 2 * ctx->cfg.capacity, 256), 256, 0, (cudaStream_t)stream>>>(
+        ctx->book(), d_out, K, ctx->cfg.capacity, ctx->lay.NP);
+    return after_launch("lob_export_book");
+}
+
+int lob_get_stats(lob_ctx *ctx, int64_t *d_out, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    if (!d_out) return fail(LOB_EINVAL, "d_out is null%s");
+    cudaError_t e = cudaMemcpyAsync(d_out, ctx->stats(), (size_t)K * NST * sizeof(long long), cudaMemcpyDeviceToDevice,
+                                    (cudaStream_t)stream);
+    return e == cudaSuccess ? LOB_OK : cuda_fail(e, "lob_get_stats copy");
+}
+
+int64_t lob_launch_count(void) { return g_launches.load(); }
+
+const char *lob_strerror(int code) {
+    switch (code) {
+        case LOB_OK: return "ok";
+        case LOB_EINVAL: return "invalid argument";
+        case LOB_ECUDA: return "CUDA error";
+        case LOB_ENOMEM: return "out of memory";
+        case LOB_EUNSUPPORTED: return "unsupported configuration";
+        default: return "unknown error";
+    }
+}
+
+const char *lob_last_error(void) { return g_err; }
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+"""Thin Python binding of the C ABI in ``include/lob.h`` (argument marshalling only).
+
+Every step of the hot path runs in ``liblob.so`` (sm_100a CUDA kernels).  PyTorch
+supplies device memory, streams and process groups; there is no CPU fallback:
+constructing a ``LobBatch`` without the built library or without a CUDA device
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblob.so")
+
+LOB_NSTATS = 10
+STAT_NAMES = ("msgs", "bad", "trades", "trades_dropped", "traded_qty", "cancelled_qty",
+              "unknown_cancels", "add_overflow", "overflow_qty", "market_discarded_qty")
+MAX_CAPACITY = 2048
+MAX_L2_LEVELS = 32
+
+_lock = threading.Lock()
+_lib = None
+
+
+class LobError(RuntimeError):
+    pass
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("n_books", ctypes.c_int32), ("capacity", ctypes.c_int32),
+                ("trades_cap", ctypes.c_int32), ("l2_levels", ctypes.c_int32),
+                ("device", ctypes.c_int32)]
+
+
+def lib():
+    """Load liblob.so (built by ``make`` / ``__graft_entry__.build()``); raise if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise LobError(f"{LIB_PATH} is missing: run `make` (or __graft_entry__.build()) first; "
+                               "there is no CPU fallback")
+            L = ctypes.CDLL(LIB_PATH)
+            P, i32 = ctypes.c_void_p, ctypes.c_int32
+            L.lob_state_bytes.restype = ctypes.c_size_t
+            L.lob_state_bytes.argtypes = [ctypes.POINTER(_Config)]
+            L.lob_create.restype = ctypes.c_int
+            L.lob_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(_Config), P]
+            L.lob_destroy.argtypes = [P]
+            L.lob_init.restype = ctypes.c_int
+            L.lob_init.argtypes = [P, P, i32, i32, i32, P]
+            L.lob_process_messages.restype = ctypes.c_int
+            L.lob_process_messages.argtypes = [P, P, i32, i32, P, P]
+            L.lob_process_messages_host.restype = ctypes.c_int
+            L.lob_process_messages_host.argtypes = [P, P, i32, i32, P, P, P, P, i32, P]
+            for name in ("lob_get_l2", "lob_get_book", "lob_get_stats"):
+                getattr(L, name).restype = ctypes.c_int
+                getattr(L, name).argtypes = [P, P, P]
+            L.lob_get_trades.restype = ctypes.c_int
+            L.lob_get_trades.argtypes = [P, P, P, P]
+            L.lob_launch_count.restype = ctypes.c_int64
+            L.lob_strerror.restype = ctypes.c_char_p
+            L.lob_strerror.argtypes = [ctypes.c_int]
+            L.lob_last_error.restype = ctypes.c_char_p
+            _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        L = lib()
+        raise LobError(f"{what}: {L.lob_strerror(rc).decode()} ({L.lob_last_error().decode()})")
+
+
+def launch_count() -> int:
+    return int(lib().lob_launch_count())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class LobBatch:
+    """K independent limit-order books of capacity N on one GPU (the C ABI's lob_ctx).
+
+    Tensors are int32 on the context's device in the layouts of include/lob.h.
+    All calls are asynchronous on torch's current stream (or ``stream=``).
+    """
+
+    def __init__(self, n_books: int, capacity: int, trades_cap: int | None = None,
+                 l2_levels: int = 10, device=None):
+        if not torch.cuda.is_available():
+            raise LobError("LobBatch needs a CUDA device; there is no CPU fallback")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.K, self.N = int(n_books), int(capacity)
+        self.T_cap = self.N if trades_cap is None else int(trades_cap)
+        self.L = int(l2_levels)
+        L = lib()
+        self._cfg = _Config(self.K, self.N, self.T_cap, self.L, self.device.index or 0)
+        nbytes = L.lob_state_bytes(ctypes.byref(self._cfg))
+        if nbytes == 0 and self.K > 0:
+            raise LobError("invalid configuration (capacity 1..2048, l2_levels 1..32, K >= 0)")
+        with torch.cuda.device(self.device):
+            self.state = torch.empty(max(int(nbytes), 256) + 256, dtype=torch.uint8, device=self.device)
+        off = (-self.state.data_ptr()) % 256
+        self._state_ptr = ctypes.c_void_p(self.state.data_ptr() + off)
+        self.ctx = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(L.lob_create(ctypes.byref(self.ctx), ctypes.byref(self._cfg), self._state_ptr),
+                   "lob_create")
+        self.last_l2 = None
+
+    def __del__(self):
+        ctx, self.ctx = getattr(self, "ctx", None), None
+        if ctx:
+            try:
+                lib().lob_destroy(ctx)
+            except Exception:
+                pass
+
+    def _dev(self, x, dtype=torch.int32):
+        if x is None:
+            return None
+        t = torch.as_tensor(x)
+        t = t.to(device=self.device, dtype=dtype, non_blocking=True)
+        return t.contiguous()
+
+    # ------------------------------------------------------------------ calls
+    def init(self, init_l2=None, init_ts: int = 0, init_tns: int = 0, stream=None):
+        """lob_init: empty books, optional synthetic L2 seed [K][L0][4]."""
+        t = self._dev(init_l2)
+        L0 = 0 if t is None else int(t.shape[1])
+        if t is not None:
+            assert t.shape == (self.K, L0, 4), t.shape
+        with torch.cuda.device(self.device):
+            _check(lib().lob_init(self.ctx, _ptr(t), L0, int(init_ts), int(init_tns), _stream(stream)),
+                   "lob_init")
+        self._keep = t  # keep the input alive until the stream has consumed it
+
+    def process(self, msgs, n_steps: int, msgs_per_step: int, l2: bool = True, l2_out=None,
+                stream=None):
+        """lob_process_messages over msgs [K][n_steps*msgs_per_step][8]; returns L2 [K][S][L][4]."""
+        m = self._dev(msgs)
+        assert m.shape == (self.K, n_steps * msgs_per_step, 8), m.shape
+        out = l2_out
+        if l2 and out is None:
+            out = torch.empty((self.K, n_steps, self.L, 4), dtype=torch.int32, device=self.device)
+        with torch.cuda.device(self.device):
+            _check(lib().lob_process_messages(self.ctx, _ptr(m), int(n_steps), int(msgs_per_step),
+                                              _ptr(out) if l2 else None, _stream(stream)),
+                   "lob_process_messages")
+        self._keep = m
+        return out if l2 else None
+
+    def process_host(self, h_msgs, n_steps: int, msgs_per_step: int, h_l2_out=None,
+                     h_stats_out=None, d_msgs_buf=None, d_l2_buf=None, chunks: int = 8, stream=None):
+        """lob_process_messages_host: pinned host messages in, pinned host L2/stats out."""
+        assert h_msgs.device.type == "cpu" and h_msgs.dtype == torch.int32 and h_msgs.is_contiguous()
+        with torch.cuda.device(self.device):
+            _check(lib().lob_process_messages_host(
+                self.ctx, _ptr(h_msgs), int(n_steps), int(msgs_per_step), _ptr(h_l2_out),
+                _ptr(h_stats_out), _ptr(d_msgs_buf), _ptr(d_l2_buf), int(chunks), _stream(stream)),
+                "lob_process_messages_host")
+
+    def l2(self, stream=None):
+        out = torch.empty((self.K, self.L, 4), dtype=torch.int32, device=self.device)
+        with torch.cuda.device(self.device):
+            _check(lib().lob_get_l2(self.ctx, _ptr(out), _stream(stream)), "lob_get_l2")
+        return out
+
+    def trades(self, stream=None):
+        out = torch.empty((self.K, self.T_cap, 6), dtype=torch.int32, device=self.device)
+        cnt = torch.empty((self.K,), dtype=torch.int32, device=self.device)
+        with torch.cuda.device(self.device):
+            _check(lib().lob_get_trades(self.ctx, _ptr(out), _ptr(cnt), _stream(stream)),
+                   "lob_get_trades")
+        return out, cnt
+
+    def book(self, stream=None):
+        out = torch.empty((self.K, 2, self.N, 6), dtype=torch.int32, device=self.device)
+        with torch.cuda.device(self.device):
+            _check(lib().lob_get_book(self.ctx, _ptr(out), _stream(stream)), "lob_get_book")
+        return out
+
+    def stats(self, stream=None):
+        out = torch.empty((self.K, LOB_NSTATS), dtype=torch.int64, device=self.device)
+        with torch.cuda.device(self.device):
+            _check(lib().lob_get_stats(self.ctx, _ptr(out), _stream(stream)), "lob_get_stats")
+        return out

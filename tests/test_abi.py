@@ -1,0 +1,87 @@
+"""CPU-side checks of the C ABI boundary (-m "not gpu"): the library loads, exports
+every symbol include/lob.h declares, sizes its state without a GPU, and fails
+loudly (never falls back to CPU) when no device is present."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "lob.h")
+PKG = os.path.join(ROOT, "paper_2308_13289_b200")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lob_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    lib_path = os.path.join(PKG, "liblob.so")
+    if not os.path.exists(lib_path):
+        subprocess.check_call(["make", "-C", ROOT, "paper_2308_13289_b200/liblob.so"])
+    import paper_2308_13289_b200 as P
+    return P.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared()
+    assert len(names) >= 12, names
+    for n in names:
+        assert hasattr(L, n), f"missing export {n}"
+    out = subprocess.check_output(["nm", "-D", "--defined-only", os.path.join(PKG, "liblob.so")]).decode()
+    for n in names:
+        assert re.search(rf"\bT {n}\b", out), n
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
+                                   os.path.join(PKG, "liblob.so")]).decode()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out), out
+
+
+def test_state_bytes_host_only(L):
+    import paper_2308_13289_b200.lob as lob
+    cfg = lob._Config(65536, 100, 512, 10, 0)
+    n = L.lob_state_bytes(ctypes.byref(cfg))
+    book = 65536 * 2 * 6 * 128 * 4
+    trades = 65536 * 512 * 24
+    assert n >= book + trades + 65536 * 4 + 65536 * 80
+    assert n < book + trades + 65536 * 4 + 65536 * 80 + 4 * 256
+    for bad in [(1, 0, 1, 10, 0), (1, 2049, 1, 10, 0), (1, 100, 1, 0, 0), (1, 100, 1, 33, 0),
+                (-1, 100, 1, 10, 0), (1, 100, -1, 10, 0)]:
+        assert L.lob_state_bytes(ctypes.byref(lob._Config(*bad))) == 0, bad
+    assert L.lob_state_bytes(None) == 0
+
+
+def test_errors_without_gpu_are_loud(L):
+    import paper_2308_13289_b200.lob as lob
+    ctx = ctypes.c_void_p()
+    cfg = lob._Config(4, 100, 10, 10, 0)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    rc = L.lob_create(ctypes.byref(ctx), ctypes.byref(cfg), ctypes.c_void_p(256))
+    assert rc == -2, rc            # LOB_ECUDA: no device, no fallback
+    assert L.lob_last_error()
+    rc = L.lob_create(ctypes.byref(ctx), ctypes.byref(lob._Config(4, 4096, 10, 10, 0)), ctypes.c_void_p(256))
+    assert rc == -4                 # LOB_EUNSUPPORTED
+    assert L.lob_init(None, None, 0, 0, 0, None) in (-1, -2)
+    with pytest.raises(lob.LobError):
+        lob.LobBatch(4, 100)
+    assert L.lob_strerror(0) == b"ok"
+
+
+def test_product_path_never_touches_the_oracle():
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in src.replace("no oracle", ""), f

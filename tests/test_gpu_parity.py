@@ -1,0 +1,149 @@
+"""GPU parity (-m gpu): the CUDA path, called through the C ABI, must equal the CPU
+oracle element by element (bit-exact: every output is integer) on the same
+seeded inputs."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import lobgen
+import oracle
+from common import STAT_NAMES, assert_outputs_equal, golden_cases, run_engine, run_golden_case
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from gpu_engine import GpuEngine, make_gpu
+
+
+def _both(cfg, n_books=None, calls=1, book_begin=0, threads=8):
+    cfg = cfg if n_books is None else cfg.with_(n_books=n_books)
+    msgs, init = lobgen.generate(cfg, book_begin=book_begin)
+    g = run_engine(GpuEngine(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels), cfg, msgs, init,
+                   lobgen.INIT_TS, lobgen.INIT_TNS, calls)
+    o = run_engine(oracle.OracleBatch(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels, threads=threads),
+                   cfg, msgs, init, lobgen.INIT_TS, lobgen.INIT_TNS, calls)
+    return g, o
+
+
+@pytest.mark.parametrize("cid,case", golden_cases(), ids=[c[0] for c in golden_cases()])
+def test_golden_on_gpu(cid, case):
+    run_golden_case(make_gpu, case)
+
+
+def test_c1_full():
+    g, o = _both(lobgen.CONFIGS["C1"])
+    assert_outputs_equal(g, o, what="C1")
+
+
+@pytest.mark.parametrize("calls", [1, 100])
+def test_c2_modes(calls):
+    # C2 at full size: mode B (one call of 100 steps) and mode A (one call per step)
+    g, o = _both(lobgen.CONFIGS["C2"], calls=calls)
+    assert_outputs_equal(g, o, what=f"C2 calls={calls}")
+
+
+@pytest.mark.parametrize("name,n", [("C3", 1000), ("C4", 1500), ("C5_32", 700), ("C5_100", 700),
+                                    ("C5_512", 150), ("C5_2048", 20)])
+def test_configs_subset(name, n):
+    # several persistent-grid waves' worth of books plus a ragged tail
+    g, o = _both(lobgen.CONFIGS[name], n_books=n)
+    assert_outputs_equal(g, o, what=name)
+
+
+@pytest.mark.parametrize("profile,N", [("ties", 100), ("overflow", 16), ("synthetic", 100),
+                                       ("garbage", 100), ("heavy_market", 64), ("lobster", 1),
+                                       ("lobster", 33), ("lobster", 97), ("overflow", 130),
+                                       ("garbage", 300), ("ties", 1024)])
+def test_profiles(profile, N):
+    cfg = lobgen.Config("p", 333, N, 7, 37, min(N, 12), 50, 10, profile, 21 + N)
+    g, o = _both(cfg)
+    assert_outputs_equal(g, o, what=f"{profile} N={N}")
+
+
+@pytest.mark.parametrize("L,Tcap", [(1, 0), (32, 3), (10, 1)])
+def test_levels_and_tiny_trade_log(L, Tcap):
+    cfg = lobgen.Config("p", 200, 100, 5, 50, 40, Tcap, L, "heavy_market", 5)
+    g, o = _both(cfg)
+    assert_outputs_equal(g, o, what=f"L={L} Tcap={Tcap}")
+
+
+def test_empty_and_degenerate_calls():
+    cfg = lobgen.Config("p", 65, 50, 3, 20, 5, 20, 5, "lobster", 8)
+    msgs, init = lobgen.generate(cfg)
+    for eng in (GpuEngine(65, 50, 20, 5), oracle.OracleBatch(65, 50, 20, 5)):
+        eng.init(init, 1, 2)
+        eng.process(msgs, 3, 20)
+        eng.process(msgs[:, :0], 0, 20)          # no messages: clears the trade log only
+    g, o = GpuEngine(65, 50, 20, 5), oracle.OracleBatch(65, 50, 20, 5)
+    for eng in (g, o):
+        eng.init(init, 1, 2)
+        eng.process(msgs, 3, 20)
+        eng.process(msgs[:, :0], 0, 20)
+    np.testing.assert_array_equal(g.book(), o.book())
+    np.testing.assert_array_equal(g.trades()[1], o.trades()[1])
+    np.testing.assert_array_equal(g.trades()[0], o.trades()[0])
+    np.testing.assert_array_equal(g.stats(), o.stats())
+    # zero books
+    z = GpuEngine(0, 100, 10, 10)
+    z.init(None)
+    z.process(np.zeros((0, 10, 8), np.int32), 1, 10)
+    assert z.book().shape == (0, 2, 100, 6)
+
+
+def test_determinism_clones_and_isolation():
+    cfg = lobgen.CONFIGS["C1"]
+    msgs, init = lobgen.generate(cfg.with_(n_books=4))
+    K = 1000
+    e = GpuEngine(K, 100, 1000, 10)
+    e.init(np.repeat(init[:1], K, 0), lobgen.INIT_TS, lobgen.INIT_TNS)
+    l2 = e.process(np.repeat(msgs[:1], K, 0), 10, 100)
+    assert (l2 == l2[:1]).all() and (e.book() == e.book()[:1]).all()
+    st = e.stats()
+    assert (st == st[:1]).all()
+
+
+def test_host_path_equals_device_path():
+    cfg = lobgen.CONFIGS["C4"].with_(n_books=3000)
+    msgs, init = lobgen.generate(cfg)
+    from paper_2308_13289_b200 import LobBatch
+    a = LobBatch(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
+    b = LobBatch(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
+    ti = torch.from_numpy(init)
+    a.init(ti, lobgen.INIT_TS, lobgen.INIT_TNS)
+    b.init(ti, lobgen.INIT_TS, lobgen.INIT_TNS)
+    l2a = a.process(torch.from_numpy(msgs), cfg.n_steps, cfg.msgs_per_step)
+    h = torch.from_numpy(msgs).pin_memory()
+    hl2 = torch.empty((cfg.n_books, cfg.n_steps, cfg.l2_levels, 4), dtype=torch.int32).pin_memory()
+    hst = torch.empty((cfg.n_books, 10), dtype=torch.int64).pin_memory()
+    dm = torch.empty_like(h, device="cuda")
+    dl = torch.empty_like(hl2, device="cuda")
+    b.process_host(h, cfg.n_steps, cfg.msgs_per_step, hl2, hst, dm, dl, chunks=5)
+    torch.cuda.synchronize()
+    assert torch.equal(hl2, l2a.cpu())
+    assert torch.equal(hst, a.stats().cpu())
+    assert torch.equal(b.book(), a.book())
+
+
+def test_full_size_c4_sampled_books():
+    """C4 at BASELINE.json's full size (65,536 books) in the launch configuration
+    bench.py times; sampled books are recomputed one by one by the oracle."""
+    cfg = lobgen.CONFIGS["C4"]
+    msgs, init = lobgen.generate(cfg)
+    e = GpuEngine(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
+    g = run_engine(e, cfg, msgs, init, lobgen.INIT_TS, lobgen.INIT_TNS)
+    rng = np.random.default_rng(0)
+    sample = np.unique(np.concatenate([[0, 1, cfg.n_books - 1], rng.integers(0, cfg.n_books, 61)]))
+    o = oracle.OracleBatch(len(sample), cfg.capacity, cfg.trades_cap, cfg.l2_levels)
+    want = run_engine(o, cfg, np.ascontiguousarray(msgs[sample]), np.ascontiguousarray(init[sample]),
+                      lobgen.INIT_TS, lobgen.INIT_TNS)
+    got = {k: v[sample] for k, v in g.items()}
+    assert_outputs_equal(got, want, what="C4 full-size sample")
+    # properties that hold at any size, on every book
+    st = g["stats"]
+    assert (st[:, STAT_NAMES.index("msgs")] == cfg.n_msgs).all()
+    assert (st[:, STAT_NAMES.index("trades")] == g["n_trades"] + st[:, STAT_NAMES.index("trades_dropped")]).all()
+    l2 = g["l2"]
+    both = (l2[..., 0] > 0) & (l2[..., 2] > 0)
+    assert (l2[..., 0, 0][both[..., 0]] > l2[..., 0, 2][both[..., 0]]).all()  # never crossed
