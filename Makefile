@@ -4,7 +4,7 @@
 #   lobgen/liblobgen.so               seeded input generator
 NVCC      ?= /usr/local/cuda/bin/nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xptxas -v -Xcompiler -fPIC,-O2 -shared
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xptxas -v -Xcompiler -fPIC,-O2 -shared
 PKG       := paper_2308_13289_b200
 LIB       := $(PKG)/liblob.so
 SRCS      := $(PKG)/csrc/lob_api.cu

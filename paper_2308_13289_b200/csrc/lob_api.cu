@@ -170,12 +170,15 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
             c->smem_bytes = 0;
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step_reg<KPL, REG_WARPS>, REG_WARPS * 32, 0);
         } else {
-            c->smem_bytes = (2 * CH * 8 + 8) * sizeof(int32_t) + (size_t)2 * NF * KPL * 32 * sizeof(int32_t);
+            c->smem_bytes = smem_step_bytes(KPL);
             e = cudaFuncSetAttribute(lob_step_smem<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)c->smem_bytes);
             if (e == cudaSuccess)
                 e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step_smem<KPL>, 32, c->smem_bytes);
         }
+        if (e == cudaSuccess && KPL * 32 * 2 * NF * 4 > 48 * 1024)
+            e = cudaFuncSetAttribute(lob_export_l2<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     KPL * 32 * 2 * NF * 4);
         if (e != cudaSuccess) rc = cuda_fail(e, "occupancy query");
     });
     if (rc != LOB_OK) { delete c; return rc; }
@@ -294,12 +297,8 @@ int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *stream) {
     if (!d_out || reinterpret_cast<uintptr_t>(d_out) % 16) return fail(LOB_EINVAL, "d_out null or misaligned%s");
     for_kpl(ctx->kpl, [&](auto kc) {
         constexpr int KPL = decltype(kc)::value;
-        if constexpr (KPL <= 4)
-            lob_export_l2_reg<KPL><<<blocks_for(K, 4), 128, 0, (cudaStream_t)stream>>>(
-                ctx->book(), d_out, K, ctx->cfg.capacity, ctx->lay.NP, ctx->cfg.l2_levels);
-        else
-            lob_export_l2_smem<KPL><<<K, 32, 0, (cudaStream_t)stream>>>(ctx->book(), d_out, K, ctx->cfg.capacity,
-                                                                          ctx->lay.NP, ctx->cfg.l2_levels);
+        lob_export_l2<KPL><<<K, 32, KPL * 32 * 2 * NF * 4, (cudaStream_t)stream>>>(
+            ctx->book(), d_out, K, ctx->cfg.capacity, ctx->lay.NP, ctx->cfg.l2_levels);
         rc = after_launch("lob_export_l2");
     });
     return rc;

@@ -1,30 +1,34 @@
 // lob_kernels.cuh -- sm_100a device code for the batched limit-order-book hot path.
 //
 // One warp owns one book (messages within a book are strictly
-// serial; books are independent).  The book's two sides (Eq.1) are
-// held in REGISTERS for capacity N <= 128 (RegBook, KPL = slots per lane) and
-// in SHARED MEMORY above that (SmemBook).  Slot i of a side lives in lane
-// (i % 32), register/row (i / 32) -- "interleaved", so that every
-// lowest-index search (free slot P:L175 / G3, order-id lookup P:L177) is a
-// ballot + find-first-set per row, and the lowest-slot tie-break of the best
-// order (G4) is the lowest set lane of the first row that has a candidate.
+// serial; books are independent).  Slot i of a side (Eq.1) lives in
+// lane (i % 32), row (i / 32) -- "interleaved" -- so that:
+//   * every lowest-index search (free slot P:L175/G3, order-id lookup P:L177,
+//     lowest-slot tie-break G4) is one lane-local scan plus ONE __reduce_min_sync
+//     over (row*32 + lane), which directly yields the warp-uniform slot;
+//   * the row of a selected slot is warp-uniform, so register writes branch
+//     on it (no per-lane select chains, no local memory).
+// Fields the method scans on every message -- P, Q, OID (Eq.2) -- are held in
+// REGISTERS for capacity N <= 128 (RegBook); the fields read only on rare
+// paths -- TID, Ts, Tns -- live in a per-warp SHARED-MEMORY region, where any
+// lane reads any slot with a broadcast load.  Above N = 128 the whole book is
+// in shared memory (SmemBook).
 //
 // Messages (Eq.6) stream HBM -> shared memory through a per-warp double buffer
-// filled by 1-D bulk async copies (cp.async.bulk, the TMA bulk path, SASS
-// UBLKCP) completing on an mbarrier; every lane reads the current message
-// with two broadcast 16-byte shared loads.  Dispatch is warp-uniform on
-// (T, S) -- the paper's 8 explicit cases -- so no lane diverges.
+// filled by 1-D bulk async copies (cp.async.bulk: the TMA bulk path, SASS
+// UBLKCP) completing on an mbarrier; every lane reads the current message with
+// two broadcast 16-byte shared loads.  Dispatch is warp-uniform on (T, S) --
+// the paper's 8 explicit cases -- so no lane diverges.
 //
-// The best standing order per side (Eq.5 + G1/G4) is cached (warp-uniform)
-// and recomputed with __reduce_min_sync / __ballot_sync only when the cached
-// order leaves the book; adds update it by one key comparison.
-//
-// Counters: lane c owns counter c (int64), so an increment is one predicated
-// add and no per-counter register is spent on every lane.
+// The best standing order of each side (Eq.5 + G1/G4) is cached (warp-uniform)
+// and recomputed with warp reductions only after the cached order leaves the
+// book; an add updates it by one key comparison.
 #pragma once
 #include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 namespace lobk {
 
@@ -35,7 +39,11 @@ enum {
     ST_MSGS = 0, ST_BAD, ST_TRADES, ST_DROPPED, ST_TRADED_QTY, ST_CANCELLED_QTY, ST_UNKNOWN,
     ST_ADD_OVF, ST_OVF_QTY, ST_DISCARDED, NST
 };
-constexpr int CH = 64;  // messages per staging chunk (2 KiB); two chunks per warp
+constexpr int CH = 32;  // messages per staging chunk (1 KiB); two chunks per warp
+constexpr int BEST_INVALID = -2, BEST_EMPTY = -1;
+
+template <int I>
+using IC = std::integral_constant<int, I>;
 
 struct Params {
     int32_t *book;         // [K][2][NF][NP] SoA, slot i at [i] (i = row*32 + lane)
@@ -76,6 +84,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// Hide how a value was computed so the register allocator keeps it instead of
+// rematerialising it (e.g. shared addresses from SR_TID / SR_CgaCtaId) in the loop.
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(x));
+    return x;
+}
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -83,65 +97,116 @@ __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// 32-bit shared-window addresses keep smem pointers in one register each (no
+// generic-pointer rematerialisation in the message loop).
+__device__ __forceinline__ int lds32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, int v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ long long lds64(uint32_t a) {
+    long long v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, long long v) {
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
 // ---------------------------------------------------------------- book storage
-// RegBook: v[s][f][j] is slot (j*32 + lane) of side s.  All indices in loops
-// are compile-time after unrolling; runtime (warp-uniform) rows go through
-// select chains so nothing spills to local memory.
+// RegBook: hot fields P, Q, OID of slot (j*32 + lane) in registers v[s][f][j];
+// cold fields TID, Ts, Tns in shared memory cold[s][f-3][NP].
 template <int KPL_>
 struct RegBook {
     static constexpr int KPL = KPL_;
-    int32_t v[2][NF][KPL_];
-    __device__ __forceinline__ int32_t at(int s, int f, int j) const { return v[s][f][j]; }
-    __device__ __forceinline__ int32_t get(int s, int f, int j) const {
-        int32_t r = v[s][f][0];
-#pragma unroll
-        for (int jj = 1; jj < KPL_; ++jj)
-            if (j == jj) r = v[s][f][jj];
-        return r;
+    static constexpr int UNR = KPL_;
+    static constexpr bool kRegs = true;
+    int32_t v[2][3][KPL_];
+    uint32_t cold;  // shared address of this warp's [2][3][NP] region
+    int lane;
+    static constexpr int cold_words() { return 2 * 3 * KPL_ * 32; }
+    __device__ __forceinline__ int32_t hot(int s, int f, int j) const { return v[s][f][j]; }
+    __device__ __forceinline__ void set_hot(int s, int f, int j, int32_t x) { v[s][f][j] = x; }
+    __device__ __forceinline__ uint32_t cold_addr(int s, int f, int slot) const {
+        return cold + 4u * (uint32_t)((s * 3 + (f - 3)) * (KPL_ * 32) + slot);
     }
-    __device__ __forceinline__ void put(int s, int f, int j, int32_t x) {
-#pragma unroll
-        for (int jj = 0; jj < KPL_; ++jj)
-            if (j == jj) v[s][f][jj] = x;
+    __device__ __forceinline__ int32_t ld(int s, int f, int slot) const { return lds32(cold_addr(s, f, slot)); }
+    __device__ __forceinline__ void st(int s, int f, int slot, int32_t x) const { sts32(cold_addr(s, f, slot), x); }
+    // run f(row) with the warp-uniform row as a compile-time constant
+    template <class F>
+    __device__ __forceinline__ void row(int j, F &&f) {
+        if constexpr (KPL_ == 1) {
+            f(IC<0>{});
+        } else {
+            switch (j) {
+                case 0: f(IC<0>{}); break;
+                case 1: f(IC<1>{}); break;
+                case 2: if constexpr (KPL_ > 2) f(IC<2>{}); break;
+                default: if constexpr (KPL_ > 3) f(IC<(KPL_ > 3 ? 3 : 0)>{}); break;
+            }
+        }
     }
-    __device__ __forceinline__ void load(const int32_t *g, int NP, int lane) {
+    __device__ __forceinline__ void load(const int32_t *g, int NP) {
 #pragma unroll
-        for (int s = 0; s < 2; ++s)
+        for (int s = 0; s < 2; ++s) {
 #pragma unroll
-            for (int f = 0; f < NF; ++f)
+            for (int f = 0; f < 3; ++f)
 #pragma unroll
                 for (int j = 0; j < KPL_; ++j) v[s][f][j] = __ldcs(g + (s * NF + f) * NP + j * 32 + lane);
+#pragma unroll
+            for (int f = 3; f < NF; ++f)
+#pragma unroll
+                for (int j = 0; j < KPL_; ++j) st(s, f, j * 32 + lane, __ldcs(g + (s * NF + f) * NP + j * 32 + lane));
+        }
+        __syncwarp();
     }
-    __device__ __forceinline__ void store(int32_t *g, int NP, int lane) const {
+    __device__ __forceinline__ void store(int32_t *g, int NP) const {
+        __syncwarp();
 #pragma unroll
         for (int s = 0; s < 2; ++s)
 #pragma unroll
             for (int j = 0; j < KPL_; ++j) {
-                const bool occ = v[s][F_Q][j] > 0;
+                const bool occ = v[s][F_Q][j] > 0;  // empty slots are all -1
 #pragma unroll
-                for (int f = 0; f < NF; ++f) __stcs(g + (s * NF + f) * NP + j * 32 + lane, occ ? v[s][f][j] : -1);
+                for (int f = 0; f < 3; ++f) __stcs(g + (s * NF + f) * NP + j * 32 + lane, occ ? v[s][f][j] : -1);
+#pragma unroll
+                for (int f = 3; f < NF; ++f)
+                    __stcs(g + (s * NF + f) * NP + j * 32 + lane, occ ? ld(s, f, j * 32 + lane) : -1);
             }
     }
 };
 
-// SmemBook: the same interleaved layout in this warp's shared-memory region.
+// SmemBook: every field in this warp's shared-memory region [2][NF][NP].
 template <int KPL_>
 struct SmemBook {
     static constexpr int KPL = KPL_;
-    int32_t *base;  // already offset by lane
-    __device__ __forceinline__ int32_t at(int s, int f, int j) const { return base[(s * NF + f) * (KPL_ * 32) + j * 32]; }
-    __device__ __forceinline__ int32_t get(int s, int f, int j) const { return at(s, f, j); }
-    __device__ __forceinline__ void put(int s, int f, int j, int32_t x) { base[(s * NF + f) * (KPL_ * 32) + j * 32] = x; }
-    __device__ __forceinline__ void load(const int32_t *g, int NP, int lane) {
-        for (int i = 0; i < 2 * NF * KPL_; ++i) base[i * 32] = g[i * 32 + lane];
+    static constexpr int UNR = 4;
+    static constexpr bool kRegs = false;
+    uint32_t cold;  // shared address of the whole book region [2][NF][NP]
+    int lane;
+    static constexpr int cold_words() { return 2 * NF * KPL_ * 32; }
+    __device__ __forceinline__ uint32_t cold_addr(int s, int f, int slot) const {
+        return cold + 4u * (uint32_t)((s * NF + f) * (KPL_ * 32) + slot);
+    }
+    __device__ __forceinline__ int32_t ld(int s, int f, int slot) const { return lds32(cold_addr(s, f, slot)); }
+    __device__ __forceinline__ void st(int s, int f, int slot, int32_t x) const { sts32(cold_addr(s, f, slot), x); }
+    __device__ __forceinline__ int32_t hot(int s, int f, int j) const { return ld(s, f, j * 32 + lane); }
+    __device__ __forceinline__ void set_hot(int s, int f, int j, int32_t x) { st(s, f, j * 32 + lane, x); }
+    template <class F>
+    __device__ __forceinline__ void row(int j, F &&f) { f(j); }
+    __device__ __forceinline__ void load(const int32_t *g, int NP) {
+        for (int i = lane; i < 2 * NF * KPL_ * 32; i += 32) sts32(cold + 4u * i, __ldcs(g + i));
         __syncwarp();
     }
-    __device__ __forceinline__ void store(int32_t *g, int NP, int lane) const {
+    __device__ __forceinline__ void store(int32_t *g, int NP) const {
         __syncwarp();
         for (int s = 0; s < 2; ++s)
             for (int j = 0; j < KPL_; ++j) {
-                const bool occ = at(s, F_Q, j) > 0;
-                for (int f = 0; f < NF; ++f) g[(s * NF + f) * NP + j * 32 + lane] = occ ? at(s, f, j) : -1;
+                const bool occ = hot(s, F_Q, j) > 0;
+                for (int f = 0; f < NF; ++f) __stcs(g + (s * NF + f) * NP + j * 32 + lane, occ ? hot(s, f, j) : -1);
             }
     }
 };
@@ -150,78 +215,97 @@ struct SmemBook {
 template <class BK>
 struct Engine {
     static constexpr int KPL = BK::KPL;
+    static constexpr int UNR = BK::UNR;
     BK bk;
     int lane, N, Tcap, ntr;
-    int32_t *tlog;  // this book's trade log [Tcap][6]
-    // warp-uniform best-order cache per side (Eq.5 + G1/G4)
-    int bslot[2], bP[2], bTS[2], bTNS[2];
-    bool bval[2];
-    long long cnt;       // lane c owns counter c
-    long long part_cxl;  // cancelled quantity accumulated on the owner lane
+    int32_t *tlog;          // this book's trade log [Tcap][6]
+    uint32_t sc;            // shared address: this warp's counters [NST] int64 (lane 0 only),
+                            // then the best orders' times bt[side][Ts, Tns] (every lane, same value)
+    // warp-uniform best-order cache per side (Eq.5 + G1/G4): slot or BEST_*, price
+    int bslot[2], bP[2];
+    long long part_cxl;     // cancelled quantity, accumulated on the owner lane (G14)
+    long long part_trd;     // traded quantity, accumulated on the owner lane
 
-    __device__ __forceinline__ void add_cnt(int c, long long x) {
-        if (lane == c) cnt += x;
+    __device__ __forceinline__ void count(int c, long long x) {  // lane 0 only
+        sts64(sc + 8u * c, lds64(sc + 8u * c) + x);
     }
-    __device__ __forceinline__ bool valid(int j) const { return j * 32 + lane < N; }
+    __device__ __forceinline__ bool valid(int j) const { return j < KPL - 1 || j * 32 + lane < N; }
+    __device__ __forceinline__ uint32_t bt_addr(int sd, int k) const { return sc + 8u * NST + 4u * (2 * sd + k); }
+
+    // Lowest slot whose lane-local predicate holds, or -1: one reduction over
+    // (row*32 + lane), which is exactly the slot index (interleaved layout).
+    template <class Pred>
+    __device__ __forceinline__ int lowest(Pred pred) const {
+        unsigned loc = 0xffffffffu;
+#pragma unroll UNR
+        for (int j = KPL - 1; j >= 0; --j)
+            if (pred(j)) loc = (unsigned)(j * 32 + lane);
+        return (int)__reduce_min_sync(FULL, loc);
+    }
 
     // Best(o_s) of side SD over occupied slots: price (ask min / bid max,
     // Eq.5 + G1), then earliest (Ts, Tns), then lowest slot (G4).
     template <int SD>
     __device__ __forceinline__ void recompute_best() {
-        int lk = INT_MAX, lts = 0, ltns = 0, lj = -1;
-#pragma unroll
+        int lk = INT_MAX;
+        bool has = false;
+#pragma unroll UNR
         for (int j = 0; j < KPL; ++j) {
-            if (bk.at(SD, F_Q, j) > 0) {
-                const int p = bk.at(SD, F_P, j);
-                const int k = (SD == ASK) ? p : ~p;  // bids: larger price = smaller key
-                const int ts = bk.at(SD, F_TS, j), tns = bk.at(SD, F_TNS, j);
-                const bool better = (lj < 0) || k < lk || (k == lk && (ts < lts || (ts == lts && tns < ltns)));
-                if (better) { lk = k; lts = ts; ltns = tns; lj = j; }
-            }
+            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+            const int k = (SD == ASK) ? p : ~p;  // bids: larger price = smaller key
+            if (q > 0) { lk = min(lk, k); has = true; }
         }
-        const bool has = lj >= 0;
-        if (!__any_sync(FULL, has)) { bval[SD] = true; bslot[SD] = -1; return; }
+        if (!__any_sync(FULL, has)) { bslot[SD] = BEST_EMPTY; return; }
         const int m = __reduce_min_sync(FULL, has ? lk : INT_MAX);
-        unsigned c = __ballot_sync(FULL, has && lk == m);
-        if (c & (c - 1)) {
-            const bool in = (c >> lane) & 1u;
-            const int t = __reduce_min_sync(FULL, in ? lts : INT_MAX);
-            c = __ballot_sync(FULL, in && lts == t);
-            if (c & (c - 1)) {
-                const bool in2 = (c >> lane) & 1u;
-                const int t2 = __reduce_min_sync(FULL, in2 ? ltns : INT_MAX);
-                c = __ballot_sync(FULL, in2 && ltns == t2);
+        // candidates at the best price: lane-local earliest (Ts, Tns, row)
+        int lts = INT_MAX, ltns = INT_MAX, lj = -1, lc = 0;
+#pragma unroll UNR
+        for (int j = 0; j < KPL; ++j) {
+            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+            const int k = (SD == ASK) ? p : ~p;
+            if (q > 0 && k == m) {
+                const int s = j * 32 + lane;
+                const int ts = bk.ld(SD, F_TS, s), tns = bk.ld(SD, F_TNS, s);
+                if (lj < 0 || ts < lts || (ts == lts && tns < ltns)) { lts = ts; ltns = tns; lj = j; }
+                ++lc;
             }
         }
+        const unsigned loc = lj < 0 ? 0xffffffffu : (unsigned)(lj * 32 + lane);
         int slot;
-        if (c & (c - 1)) {
-            const bool in3 = (c >> lane) & 1u;
-            slot = (int)__reduce_min_sync(FULL, in3 ? (unsigned)(lj * 32 + lane) : 0xffffffffu);
+        if (__reduce_add_sync(FULL, (unsigned)lc) == 1) {
+            slot = (int)__reduce_min_sync(FULL, loc);
         } else {
-            const int w = __ffs(c) - 1;
-            slot = __shfl_sync(FULL, lj, w) * 32 + w;
+            const bool in = lj >= 0;
+            const int t = __reduce_min_sync(FULL, in ? lts : INT_MAX);
+            const bool in2 = in && lts == t;
+            const int t2 = __reduce_min_sync(FULL, in2 ? ltns : INT_MAX);
+            slot = (int)__reduce_min_sync(FULL, (in2 && ltns == t2) ? loc : 0xffffffffu);
         }
-        const int w = slot & 31;
         bslot[SD] = slot;
         bP[SD] = (SD == ASK) ? m : ~m;
-        bTS[SD] = __shfl_sync(FULL, lts, w);
-        bTNS[SD] = __shfl_sync(FULL, ltns, w);
-        bval[SD] = true;
+        sts32(bt_addr(SD, 0), bk.ld(SD, F_TS, slot));   // broadcast shared loads
+        sts32(bt_addr(SD, 1), bk.ld(SD, F_TNS, slot));
     }
 
     // A new order at `slot` on side SD: keep the cache exact (G4 key order).
     template <int SD>
     __device__ __forceinline__ void note_add(int slot, int p, int ts, int tns) {
-        if (!bval[SD]) return;
-        if (bslot[SD] < 0) {
-            bslot[SD] = slot; bP[SD] = p; bTS[SD] = ts; bTNS[SD] = tns;
-            return;
+        const int bs = bslot[SD];
+        if (bs == BEST_INVALID) return;
+        bool better = bs == BEST_EMPTY;
+        if (!better) {
+            const int kn = (SD == ASK) ? p : ~p, kb = (SD == ASK) ? bP[SD] : ~bP[SD];
+            better = kn < kb;
+            if (kn == kb) {                      // same price: time, then slot (G4)
+                const int bts = lds32(bt_addr(SD, 0)), btns = lds32(bt_addr(SD, 1));
+                better = ts < bts || (ts == bts && (tns < btns || (tns == btns && slot < bs)));
+            }
         }
-        const int kn = (SD == ASK) ? p : ~p, kb = (SD == ASK) ? bP[SD] : ~bP[SD];
-        const bool better =
-            kn < kb ||
-            (kn == kb && (ts < bTS[SD] || (ts == bTS[SD] && (tns < bTNS[SD] || (tns == bTNS[SD] && slot < bslot[SD])))));
-        if (better) { bslot[SD] = slot; bP[SD] = p; bTS[SD] = ts; bTNS[SD] = tns; }
+        if (better) {
+            bslot[SD] = slot; bP[SD] = p;
+            sts32(bt_addr(SD, 0), ts);
+            sts32(bt_addr(SD, 1), tns);
+        }
     }
 
     // Cancellation (cancel == delete P:L289): lowest occupied slot with
@@ -229,104 +313,111 @@ struct Engine {
     // order (OID <= -9000, G12) at the message price.
     template <int SD>
     __device__ __forceinline__ void cancel(int mQ, int mP, int mOID) {
-        if (mQ <= 0) { add_cnt(ST_BAD, 1); return; }  // G22
-        int slot = -1;
-#pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            const unsigned f = __ballot_sync(FULL, bk.at(SD, F_Q, j) > 0 && bk.at(SD, F_OID, j) == mOID);
-            if (slot < 0 && f) slot = j * 32 + __ffs(f) - 1;
-        }
-        if (slot < 0) {
-#pragma unroll
-            for (int j = 0; j < KPL; ++j) {
-                const unsigned f = __ballot_sync(FULL, bk.at(SD, F_Q, j) > 0 && bk.at(SD, F_OID, j) <= -9000 &&
-                                                           bk.at(SD, F_P, j) == mP);
-                if (slot < 0 && f) slot = j * 32 + __ffs(f) - 1;
+        if (mQ <= 0) { if (lane == 0) count(ST_BAD, 1); return; }  // G22
+        int slot = lowest([&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
+        if (slot < 0)
+            slot = lowest([&](int j) {
+                return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
+            });
+        if (slot < 0) { if (lane == 0) count(ST_UNKNOWN, 1); return; }  // G15
+        const bool own = lane == (slot & 31);
+        bk.row(slot >> 5, [&](auto J) {
+            if (own) {
+                const int qi = bk.hot(SD, F_Q, J);
+                part_cxl += (mQ < qi) ? mQ : qi;               // G14
+                bk.set_hot(SD, F_Q, J, qi - mQ);               // Q <= 0 -> empty
             }
-        }
-        if (slot < 0) { add_cnt(ST_UNKNOWN, 1); return; }  // G15
-        const int oj = slot >> 5;
-        if (lane == (slot & 31)) {
-            const int qi = bk.get(SD, F_Q, oj);
-            part_cxl += (mQ < qi) ? mQ : qi;  // G14
-            bk.put(SD, F_Q, oj, qi - mQ);     // Q <= 0 -> empty
-        }
-        if (bval[SD] && bslot[SD] == slot) bval[SD] = false;
+        });
+        if (bslot[SD] == slot) bslot[SD] = BEST_INVALID;
+        if constexpr (!BK::kRegs) __syncwarp();
     }
 
     // Limit (T=1) or market (T=4) order of side OWN.
-    template <int OWN, bool MARKET>
-    __device__ __forceinline__ void aggress(int mQ, int mP, int mOID, int mTID, int mTS, int mTNS) {
+    template <int OWN>
+    __device__ __forceinline__ void aggress(bool market, int mQ, int mP, int mOID, int mTID, int mTS, int mTNS) {
         constexpr int OPP = 1 - OWN;
-        if (!MARKET && mP <= 0) { add_cnt(ST_BAD, 1); return; }  // G22
-        const int Pa = MARKET ? (OWN == BID ? INT_MAX : 0) : mP;   // P_m = 0 / max_int (G18)
+        if (!market && mP <= 0) { if (lane == 0) count(ST_BAD, 1); return; }  // G22
+        const int Pa = market ? (OWN == BID ? INT_MAX : 0) : mP;  // P_m = 0 / max_int (G18)
         int Qa = mQ;
         while (Qa > 0) {
-            if (!bval[OPP]) recompute_best<OPP>();
-            if (bslot[OPP] < 0) break;                              // side empty
+            if (bslot[OPP] == BEST_INVALID) recompute_best<OPP>();
+            const int s = bslot[OPP];
+            if (s < 0) break;                                       // side empty
             const int Ps = bP[OPP];
             if (OWN == BID ? (Pa < Ps) : (Pa > Ps)) break;          // prices do not overlap
-            const int s = bslot[OPP], ol = s & 31, oj = s >> 5;
-            const int Qs = __shfl_sync(FULL, bk.get(OPP, F_Q, oj), ol);
+            const int ol = s & 31;
+            const bool own = lane == ol;
+            int Qs, myoid;
+            if constexpr (BK::kRegs) {   // the owner's registers; Q broadcast by shuffle
+                int myq = 0;
+                myoid = 0;
+                bk.row(s >> 5, [&](auto J) { myq = bk.hot(OPP, F_Q, J); myoid = bk.hot(OPP, F_OID, J); });
+                Qs = __shfl_sync(FULL, myq, ol);
+            } else {                     // shared memory: every lane reads the slot
+                Qs = bk.ld(OPP, F_Q, s);
+                myoid = bk.ld(OPP, F_OID, s);
+            }
             const int Qs2 = (Qs - Qa > 0) ? (Qs - Qa) : 0;            // Q_s' = max(0, Q_s - Q_a)
             const int q = Qs - Qs2;                                   // Q_j = Q_s - Q_s'
             Qa = Qa - Qs;                                             // Q_a' = Q_a - Q_s
-            if (ntr < Tcap) {                                         // Eq.3 record, Eq.4 cap (G8)
-                if (lane == ol) {
+            if (own) {
+                if (ntr < Tcap) {                                     // Eq.3 record, Eq.4 cap (G8)
                     int2 *t = reinterpret_cast<int2 *>(tlog + (size_t)ntr * 6);
                     t[0] = make_int2(Ps, q);
-                    t[1] = make_int2(mOID, bk.get(OPP, F_OID, oj));
+                    t[1] = make_int2(mOID, myoid);
                     t[2] = make_int2(mTS, mTNS);
                 }
-                ++ntr;
-            } else {
-                add_cnt(ST_DROPPED, 1);
+                part_trd += q;
             }
-            add_cnt(ST_TRADED_QTY, q);
-            if (lane == ol) bk.put(OPP, F_Q, oj, Qs2);              // filled order removed (G10)
-            if (Qs2 == 0) bval[OPP] = false;
+            ++ntr;                                                    // fills this call (logged = min(ntr, Tcap))
+            bk.row(s >> 5, [&](auto J) {
+                if (own) bk.set_hot(OPP, F_Q, J, Qs2);               // filled order removed (G10)
+            });
+            if (Qs2 == 0) bslot[OPP] = BEST_INVALID;
+            if constexpr (!BK::kRegs) __syncwarp();
         }
-        if (!MARKET) {
-            if (Qa > 0) {                                            // remainder rests
-                int slot = -1;
-#pragma unroll
-                for (int j = 0; j < KPL; ++j) {
-                    const unsigned f = __ballot_sync(FULL, valid(j) && bk.at(OWN, F_Q, j) <= 0);
-                    if (slot < 0 && f) slot = j * 32 + __ffs(f) - 1;  // lowest empty slot (G3)
-                }
-                if (slot < 0) {                                      // side saturated (G6)
-                    add_cnt(ST_ADD_OVF, 1);
-                    add_cnt(ST_OVF_QTY, Qa);
-                } else {
-                    const int oj = slot >> 5;
-                    if (lane == (slot & 31)) {                       // G27
-                        bk.put(OWN, F_P, oj, mP); bk.put(OWN, F_Q, oj, Qa); bk.put(OWN, F_OID, oj, mOID);
-                        bk.put(OWN, F_TID, oj, mTID); bk.put(OWN, F_TS, oj, mTS); bk.put(OWN, F_TNS, oj, mTNS);
-                    }
-                    note_add<OWN>(slot, mP, mTS, mTNS);
-                }
+        if (Qa <= 0) return;
+        if (market) {
+            if (lane == 0) count(ST_DISCARDED, Qa);
+            return;
+        }
+        // remainder rests as one new order in the lowest empty slot (G3)
+        const int slot = lowest([&](int j) { return valid(j) && bk.hot(OWN, F_Q, j) <= 0; });
+        if (slot < 0) {                                              // side saturated (G6)
+            if (lane == 0) { count(ST_ADD_OVF, 1); count(ST_OVF_QTY, Qa); }
+            return;
+        }
+        const bool own = lane == (slot & 31);
+        bk.row(slot >> 5, [&](auto J) {                              // G27
+            if (own) {
+                bk.set_hot(OWN, F_P, J, mP);
+                bk.set_hot(OWN, F_Q, J, Qa);
+                bk.set_hot(OWN, F_OID, J, mOID);
             }
-        } else if (Qa > 0) {
-            add_cnt(ST_DISCARDED, Qa);
-        }
+        });
+        // every lane stores the same value, so each lane later reads its own write
+        bk.st(OWN, F_TID, slot, mTID);
+        bk.st(OWN, F_TS, slot, mTS);
+        bk.st(OWN, F_TNS, slot, mTNS);
+        if constexpr (!BK::kRegs) __syncwarp();
+        note_add<OWN>(slot, mP, mTS, mTNS);
     }
 
     __device__ __forceinline__ void message(const int4 a, const int4 b) {
         const int T = a.x, S = a.y, Q = a.z, P = a.w;
         if (T == 0) return;                                          // padding (G21)
+        // T in 1..4 and S in {-1, +1}, else malformed (G22)
+        if (!(((unsigned)(T - 1) < 4u) & ((((unsigned)(S + 1)) & ~2u) == 0u))) {
+            if (lane == 0) count(ST_BAD, 1);
+            return;
+        }
         // the paper's 8 (type x side) cases; cancel and delete share one
-        const unsigned t = (unsigned)(T - 1);
-        const int c = (S == 1) ? 0 : (S == -1) ? 1 : 2;
-        if (t > 3u || c == 2) { add_cnt(ST_BAD, 1); return; }          // G22
-        switch (t * 2 + c) {
-            case 0: aggress<BID, false>(Q, P, b.x, b.y, b.z, b.w); break;
-            case 1: aggress<ASK, false>(Q, P, b.x, b.y, b.z, b.w); break;
-            case 2:
-            case 4: cancel<BID>(Q, P, b.x); break;
-            case 3:
-            case 5: cancel<ASK>(Q, P, b.x); break;
-            case 6: aggress<BID, true>(Q, P, b.x, b.y, b.z, b.w); break;
-            default: aggress<ASK, true>(Q, P, b.x, b.y, b.z, b.w); break;
+        if ((unsigned)(T - 2) < 2u) {
+            if (S == 1) cancel<BID>(Q, P, b.x);
+            else cancel<ASK>(Q, P, b.x);
+        } else {
+            if (S == 1) aggress<BID>(T == 4, Q, P, b.x, b.y, b.z, b.w);
+            else aggress<ASK>(T == 4, Q, P, b.x, b.y, b.z, b.w);
         }
     }
 
@@ -340,22 +431,20 @@ struct Engine {
         for (int k = 0; k < L; ++k) {
             int lk = INT_MAX;
             bool lf = false;
-#pragma unroll
+#pragma unroll UNR
             for (int j = 0; j < KPL; ++j) {
-                if (bk.at(SD, F_Q, j) > 0) {
-                    const int p = bk.at(SD, F_P, j);
-                    const int key = (SD == ASK) ? p : ~p;
-                    if ((!have_prev || key > prev) && (!lf || key < lk)) { lk = key; lf = true; }
-                }
+                const int p = bk.hot(SD, F_P, j);
+                const int key = (SD == ASK) ? p : ~p;
+                if (bk.hot(SD, F_Q, j) > 0 && (!have_prev || key > prev)) { lk = min(lk, key); lf = true; }
             }
             if (!__any_sync(FULL, lf)) break;
             const int m = __reduce_min_sync(FULL, lf ? lk : INT_MAX);
             unsigned lq = 0;
-#pragma unroll
+#pragma unroll UNR
             for (int j = 0; j < KPL; ++j) {
-                const int p = bk.at(SD, F_P, j);
+                const int p = bk.hot(SD, F_P, j);
                 const int key = (SD == ASK) ? p : ~p;
-                if (bk.at(SD, F_Q, j) > 0 && key == m) lq += (unsigned)bk.at(SD, F_Q, j);
+                if (bk.hot(SD, F_Q, j) > 0 && key == m) lq += (unsigned)bk.hot(SD, F_Q, j);
             }
             const unsigned qs = __reduce_add_sync(FULL, lq);
             if (lane == k) { outp = (SD == ASK) ? m : ~m; outq = (int)qs; }
@@ -372,15 +461,20 @@ struct Engine {
 };
 
 // ------------------------------------------------------------------ step kernel
+// Per-warp shared scratch: counters [NST] int64 + best times [2][2] int32.
+constexpr int SCRATCH_BYTES = 8 * NST + 16;
+
 // Persistent: each warp walks books w, w + total_warps, ...
 template <class BK, int WARPS>
 __device__ __forceinline__ void run_books(const Params &p, BK &bk, int32_t *stage /*[2][CH][8]*/, uint64_t *bars,
-                                          uint32_t &chunk_seq) {
-    const int lane = threadIdx.x & 31;
+                                          uint32_t scratch) {
+    const int lane = (int)opaque(threadIdx.x & 31);
     const int gw = blockIdx.x * WARPS + (threadIdx.x >> 5);
     const int nw = gridDim.x * WARPS;
     const int nmsg = p.n_steps * p.M;
     const int nchunks = (nmsg + CH - 1) / CH;
+    uint32_t chunk_seq = 0;
+    const uint32_t stage_u32 = opaque(smem_u32(stage));
     for (int lb = gw; lb < p.nb; lb += nw) {
         const int b = p.book0 + lb;
         const int4 *src = reinterpret_cast<const int4 *>(p.msgs + (size_t)lb * nmsg * 8);
@@ -398,23 +492,27 @@ __device__ __forceinline__ void run_books(const Params &p, BK &bk, int32_t *stag
                 }
             }
         }
+        if (lane < NST) sts64(scratch + 8u * lane, 0);
         Engine<BK> e;
         e.bk = bk;
-        e.bk.load(p.book + (size_t)b * 2 * NF * p.NP, p.NP, lane);
-        e.lane = lane; e.N = p.N; e.Tcap = p.Tcap; e.ntr = 0;
+        e.bk.load(p.book + (size_t)b * 2 * NF * p.NP, p.NP);
+        e.lane = lane; e.N = p.N; e.Tcap = p.Tcap; e.ntr = 0; e.sc = scratch;
         e.tlog = p.trades + (size_t)b * p.Tcap * 6;
-        e.bval[0] = e.bval[1] = false;
-        e.bslot[0] = e.bslot[1] = -1;
-        e.bP[0] = e.bP[1] = e.bTS[0] = e.bTS[1] = e.bTNS[0] = e.bTNS[1] = 0;
-        e.cnt = 0; e.part_cxl = 0;
+        e.bslot[0] = e.bslot[1] = BEST_INVALID;
+        e.bP[0] = e.bP[1] = 0;
+        e.part_cxl = 0; e.part_trd = 0;
         int left = p.M, step = 0;
         for (int c = 0; c < nchunks; ++c) {
             const uint32_t seq = chunk_seq + c, slot = seq & 1;
             mbar_wait(&bars[slot], (seq >> 1) & 1);
-            const int4 *buf = reinterpret_cast<const int4 *>(stage + slot * CH * 8);
+            uint32_t maddr = stage_u32 + slot * CH * 32;
             const int cnt = min(CH, nmsg - c * CH);
-            for (int i = 0; i < cnt; ++i) {
-                const int4 a = buf[2 * i], bb = buf[2 * i + 1];
+            for (int i = 0; i < cnt; ++i, maddr += 32) {
+                int4 a, bb;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(maddr));
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4+16];"
+                             : "=r"(bb.x), "=r"(bb.y), "=r"(bb.z), "=r"(bb.w) : "r"(maddr));
                 e.message(a, bb);
                 if (--left == 0) {                     // end of a step: L2 snapshot (G23)
                     left = p.M;
@@ -432,24 +530,38 @@ __device__ __forceinline__ void run_books(const Params &p, BK &bk, int32_t *stag
         }
         chunk_seq += nchunks;
         // writeback: book, trade count, counters (msgs += nmsg; trades = logged + dropped)
-        e.bk.store(p.book + (size_t)b * 2 * NF * p.NP, p.NP, lane);
-        long long cx = e.part_cxl;
+        e.bk.store(p.book + (size_t)b * 2 * NF * p.NP, p.NP);
+        long long cx = e.part_cxl, tq = e.part_trd;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cx += __shfl_xor_sync(FULL, cx, o);
-        const long long dropped = __shfl_sync(FULL, e.cnt, ST_DROPPED);
-        if (lane == ST_CANCELLED_QTY) e.cnt += cx;
-        if (lane == ST_MSGS) e.cnt += nmsg;
-        if (lane == ST_TRADES) e.cnt += e.ntr + dropped;
-        if (lane < NST) p.stats[(size_t)b * NST + lane] += e.cnt;
-        if (lane == 0) p.ntrades[b] = e.ntr;
-        bk = e.bk;  // keep the smem base pointer for the next book
+        for (int o = 16; o > 0; o >>= 1) {
+            cx += __shfl_xor_sync(FULL, cx, o);
+            tq += __shfl_xor_sync(FULL, tq, o);
+        }
+        __syncwarp();
+        const int logged = min(e.ntr, p.Tcap);
+        if (lane < NST) {
+            long long v = lds64(scratch + 8u * lane);
+            if (lane == ST_CANCELLED_QTY) v += cx;
+            if (lane == ST_TRADED_QTY) v += tq;
+            if (lane == ST_DROPPED) v += e.ntr - logged;
+            if (lane == ST_MSGS) v += nmsg;
+            if (lane == ST_TRADES) v += e.ntr;             // fills = logged + dropped
+            p.stats[(size_t)b * NST + lane] += v;
+        }
+        if (lane == 0) p.ntrades[b] = logged;
     }
 }
 
+// minimum resident CTAs per SM: caps registers without spills
+#ifndef MINB_REG
+#define MINB_REG 6
+#endif
 template <int KPL, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) lob_step_reg(const Params p) {
+__global__ void __launch_bounds__(WARPS * 32, (KPL <= 2 ? 8 : MINB_REG)) lob_step_reg(const Params p) {
     __shared__ __align__(128) int32_t stage[WARPS][2][CH][8];
+    __shared__ __align__(16) int32_t cold[WARPS][RegBook<KPL>::cold_words()];
     __shared__ __align__(8) uint64_t bars[WARPS][2];
+    __shared__ __align__(16) unsigned char scratch[WARPS][SCRATCH_BYTES];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
         mbar_init(&bars[w][0], 1);
@@ -457,9 +569,10 @@ __global__ void __launch_bounds__(WARPS * 32) lob_step_reg(const Params p) {
         fence_mbar_init();
     }
     __syncwarp();
-    uint32_t seq = 0;
     RegBook<KPL> bk;
-    run_books<RegBook<KPL>, WARPS>(p, bk, &stage[w][0][0][0], bars[w], seq);
+    bk.cold = opaque(smem_u32(cold[w]));
+    bk.lane = (int)opaque(lane);
+    run_books<RegBook<KPL>, WARPS>(p, bk, &stage[w][0][0][0], bars[w], opaque(smem_u32(scratch[w])));
 }
 
 template <int KPL>
@@ -467,7 +580,8 @@ __global__ void __launch_bounds__(32) lob_step_smem(const Params p) {
     extern __shared__ __align__(128) int32_t dyn[];
     int32_t *stage = dyn;                                          // [2][CH][8]
     uint64_t *bars = reinterpret_cast<uint64_t *>(dyn + 2 * CH * 8);
-    int32_t *bookmem = dyn + 2 * CH * 8 + 8;                       // [2][NF][KPL*32]
+    const uint32_t scratch = opaque(smem_u32(dyn + 2 * CH * 8 + 4));  // SCRATCH_BYTES
+    int32_t *bookmem = dyn + 2 * CH * 8 + 4 + SCRATCH_BYTES / 4;  // [2][NF][KPL*32]
     const int lane = threadIdx.x & 31;
     if (lane == 0) {
         mbar_init(&bars[0], 1);
@@ -475,11 +589,12 @@ __global__ void __launch_bounds__(32) lob_step_smem(const Params p) {
         fence_mbar_init();
     }
     __syncwarp();
-    uint32_t seq = 0;
     SmemBook<KPL> bk;
-    bk.base = bookmem + lane;
-    run_books<SmemBook<KPL>, 1>(p, bk, stage, bars, seq);
+    bk.cold = opaque(smem_u32(bookmem));
+    bk.lane = lane;
+    run_books<SmemBook<KPL>, 1>(p, bk, stage, bars, scratch);
 }
+constexpr int smem_step_bytes(int kpl) { return (2 * CH * 8 + 4) * 4 + SCRATCH_BYTES + 2 * NF * kpl * 32 * 4; }
 
 // ------------------------------------------------------------- init / exports
 // a0: -1 everywhere, counters 0, then one synthetic order per
@@ -545,25 +660,18 @@ __global__ void lob_export_trades(const int32_t *trades, const int32_t *ntrades,
     if (counts && t < K) counts[t] = ntrades[t];
 }
 
-// current L2 of every book, computed from the stored state (warp per book)
+// current L2 of every book from the stored state: one warp per book, book in smem
 template <int KPL>
-__global__ void lob_export_l2_reg(const int32_t *book, int32_t *out, int K, int N, int NP, int L) {
-    const int lane = threadIdx.x & 31;
-    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (b >= K) return;
-    Engine<RegBook<KPL>> e;
-    e.lane = lane; e.N = N;
-    e.bk.load(book + (size_t)b * 2 * NF * NP, NP, lane);
-    e.l2_write(out + (size_t)b * L * 4, L);
-}
-template <int KPL>
-__global__ void lob_export_l2_smem(const int32_t *book, int32_t *out, int K, int N, int NP, int L) {
+__global__ void __launch_bounds__(32) lob_export_l2(const int32_t *book, int32_t *out, int K, int N, int NP, int L) {
+    extern __shared__ __align__(16) int32_t bookmem[];
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.x;
     if (b >= K) return;
     Engine<SmemBook<KPL>> e;
     e.lane = lane; e.N = N;
-    e.bk.base = const_cast<int32_t *>(book) + (size_t)b * 2 * NF * NP + lane;  // read in place (global)
+    e.bk.cold = smem_u32(bookmem);
+    e.bk.lane = lane;
+    e.bk.load(book + (size_t)b * 2 * NF * NP, NP);
     e.l2_write(out + (size_t)b * L * 4, L);
 }
 

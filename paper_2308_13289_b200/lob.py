@@ -14,7 +14,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblob.so")
+LIB_PATH = os.environ.get("LOB_LIB_OVERRIDE") or os.path.join(_HERE, "liblob.so")  # override: A/B experiments
 
 LOB_NSTATS = 10
 STAT_NAMES = ("msgs", "bad", "trades", "trades_dropped", "traded_qty", "cancelled_qty",

@@ -16,7 +16,8 @@ import sys
 import tempfile
 
 rep, fn = sys.argv[1], sys.argv[2]
-top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+dump = len(sys.argv) > 3 and sys.argv[3] == "dump"
+top = int(sys.argv[3]) if len(sys.argv) > 3 and not dump else 40
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 so = os.path.join(root, "paper_2308_13289_b200", "liblob.so")
 
@@ -66,6 +67,13 @@ for l in dis[start + 1:]:
             pending = []
         line_of[int(m.group(1), 16)] = (cur_inner, cur_outer, m.group(2).split(";")[0].strip())
 
+if dump:
+    thr, norm = float(sys.argv[4]), float(sys.argv[5])
+    for a in sorted(counts):
+        if counts[a] >= thr:
+            li = line_of.get(a, (None, None, ""))
+            print(f"{a:06x} {counts[a] / norm:7.3f} {str(li[0][1]) if li[0] else '-':>4s} {li[2][:100]}")
+    sys.exit(0)
 src = open(os.path.join(root, "paper_2308_13289_b200", "csrc", "lob_kernels.cuh")).read().splitlines()
 agg_i, agg_s = collections.Counter(), collections.Counter()
 total = sum(counts.values())
