@@ -116,25 +116,41 @@ __device__ __forceinline__ void sts64(uint32_t a, long long v) {
     asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ int2 lds64x2(uint32_t a) {
+    int2 v;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int4 lds128(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, int4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 // ---------------------------------------------------------------- book storage
 // RegBook: hot fields P, Q, OID of slot (j*32 + lane) in registers v[s][f][j];
-// cold fields TID, Ts, Tns in shared memory cold[s][f-3][NP].
+// cold fields in shared memory, one 16-byte record per slot: cold[s][slot] =
+// {Ts, Tns, TID, 0}, so an add is one vector store and a time read one load.
 template <int KPL_>
 struct RegBook {
     static constexpr int KPL = KPL_;
     static constexpr int UNR = KPL_;
     static constexpr bool kRegs = true;
     int32_t v[2][3][KPL_];
-    uint32_t cold;  // shared address of this warp's [2][3][NP] region
+    uint32_t cold;  // shared address of this warp's [2][NP][4] region
     int lane;
-    static constexpr int cold_words() { return 2 * 3 * KPL_ * 32; }
+    static constexpr int cold_words() { return 2 * KPL_ * 32 * 4; }
     __device__ __forceinline__ int32_t hot(int s, int f, int j) const { return v[s][f][j]; }
     __device__ __forceinline__ void set_hot(int s, int f, int j, int32_t x) { v[s][f][j] = x; }
-    __device__ __forceinline__ uint32_t cold_addr(int s, int f, int slot) const {
-        return cold + 4u * (uint32_t)((s * 3 + (f - 3)) * (KPL_ * 32) + slot);
+    __device__ __forceinline__ uint32_t rec(int s, int slot) const { return cold + 16u * (uint32_t)(s * KPL_ * 32 + slot); }
+    __device__ __forceinline__ int2 times(int s, int slot) const { return lds64x2(rec(s, slot)); }
+    __device__ __forceinline__ void put_cold(int s, int slot, int tid, int ts, int tns) const {
+        sts128(rec(s, slot), make_int4(ts, tns, tid, 0));
     }
-    __device__ __forceinline__ int32_t ld(int s, int f, int slot) const { return lds32(cold_addr(s, f, slot)); }
-    __device__ __forceinline__ void st(int s, int f, int slot, int32_t x) const { sts32(cold_addr(s, f, slot), x); }
     // run f(row) with the warp-uniform row as a compile-time constant
     template <class F>
     __device__ __forceinline__ void row(int j, F &&f) {
@@ -149,6 +165,18 @@ struct RegBook {
             }
         }
     }
+    // value of field f in row j (warp-uniform j), branch-free select chain
+    __device__ __forceinline__ int32_t get(int s, int f, int j) const {
+        int32_t r = v[s][f][0];
+#pragma unroll
+        for (int jj = 1; jj < KPL_; ++jj) r = (j == jj) ? v[s][f][jj] : r;
+        return r;
+    }
+    __device__ __forceinline__ void put_if(bool pred, int s, int f, int j, int32_t x) {
+#pragma unroll
+        for (int jj = 0; jj < KPL_; ++jj)
+            if (pred && j == jj) v[s][f][jj] = x;
+    }
     __device__ __forceinline__ void load(const int32_t *g, int NP) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
@@ -157,9 +185,10 @@ struct RegBook {
 #pragma unroll
                 for (int j = 0; j < KPL_; ++j) v[s][f][j] = __ldcs(g + (s * NF + f) * NP + j * 32 + lane);
 #pragma unroll
-            for (int f = 3; f < NF; ++f)
-#pragma unroll
-                for (int j = 0; j < KPL_; ++j) st(s, f, j * 32 + lane, __ldcs(g + (s * NF + f) * NP + j * 32 + lane));
+            for (int j = 0; j < KPL_; ++j) {
+                const int *r = g + s * NF * NP + j * 32 + lane;
+                put_cold(s, j * 32 + lane, __ldcs(r + F_TID * NP), __ldcs(r + F_TS * NP), __ldcs(r + F_TNS * NP));
+            }
         }
         __syncwarp();
     }
@@ -170,11 +199,13 @@ struct RegBook {
 #pragma unroll
             for (int j = 0; j < KPL_; ++j) {
                 const bool occ = v[s][F_Q][j] > 0;  // empty slots are all -1
+                int *r = g + s * NF * NP + j * 32 + lane;
 #pragma unroll
-                for (int f = 0; f < 3; ++f) __stcs(g + (s * NF + f) * NP + j * 32 + lane, occ ? v[s][f][j] : -1);
-#pragma unroll
-                for (int f = 3; f < NF; ++f)
-                    __stcs(g + (s * NF + f) * NP + j * 32 + lane, occ ? ld(s, f, j * 32 + lane) : -1);
+                for (int f = 0; f < 3; ++f) __stcs(r + f * NP, occ ? v[s][f][j] : -1);
+                const int4 c = lds128(rec(s, j * 32 + lane));
+                __stcs(r + F_TID * NP, occ ? c.z : -1);
+                __stcs(r + F_TS * NP, occ ? c.x : -1);
+                __stcs(r + F_TNS * NP, occ ? c.y : -1);
             }
     }
 };
@@ -195,6 +226,14 @@ struct SmemBook {
     __device__ __forceinline__ void st(int s, int f, int slot, int32_t x) const { sts32(cold_addr(s, f, slot), x); }
     __device__ __forceinline__ int32_t hot(int s, int f, int j) const { return ld(s, f, j * 32 + lane); }
     __device__ __forceinline__ void set_hot(int s, int f, int j, int32_t x) { st(s, f, j * 32 + lane, x); }
+    __device__ __forceinline__ int2 times(int s, int slot) const { return make_int2(ld(s, F_TS, slot), ld(s, F_TNS, slot)); }
+    __device__ __forceinline__ void put_cold(int s, int slot, int tid, int ts, int tns) const {
+        st(s, F_TID, slot, tid); st(s, F_TS, slot, ts); st(s, F_TNS, slot, tns);
+    }
+    __device__ __forceinline__ int32_t get(int s, int f, int j) const { return hot(s, f, j); }
+    __device__ __forceinline__ void put_if(bool pred, int s, int f, int j, int32_t x) {
+        if (pred) set_hot(s, f, j, x);
+    }
     template <class F>
     __device__ __forceinline__ void row(int j, F &&f) { f(j); }
     __device__ __forceinline__ void load(const int32_t *g, int NP) {
@@ -265,7 +304,8 @@ struct Engine {
             const int k = (SD == ASK) ? p : ~p;
             if (q > 0 && k == m) {
                 const int s = j * 32 + lane;
-                const int ts = bk.ld(SD, F_TS, s), tns = bk.ld(SD, F_TNS, s);
+                const int2 t2 = bk.times(SD, s);
+                const int ts = t2.x, tns = t2.y;
                 if (lj < 0 || ts < lts || (ts == lts && tns < ltns)) { lts = ts; ltns = tns; lj = j; }
                 ++lc;
             }
@@ -283,8 +323,9 @@ struct Engine {
         }
         bslot[SD] = slot;
         bP[SD] = (SD == ASK) ? m : ~m;
-        sts32(bt_addr(SD, 0), bk.ld(SD, F_TS, slot));   // broadcast shared loads
-        sts32(bt_addr(SD, 1), bk.ld(SD, F_TNS, slot));
+        const int2 bt = bk.times(SD, slot);              // broadcast shared load
+        sts32(bt_addr(SD, 0), bt.x);
+        sts32(bt_addr(SD, 1), bt.y);
     }
 
     // A new order at `slot` on side SD: keep the cache exact (G4 key order).
@@ -321,13 +362,10 @@ struct Engine {
             });
         if (slot < 0) { if (lane == 0) count(ST_UNKNOWN, 1); return; }  // G15
         const bool own = lane == (slot & 31);
-        bk.row(slot >> 5, [&](auto J) {
-            if (own) {
-                const int qi = bk.hot(SD, F_Q, J);
-                part_cxl += (mQ < qi) ? mQ : qi;               // G14
-                bk.set_hot(SD, F_Q, J, qi - mQ);               // Q <= 0 -> empty
-            }
-        });
+        const int j = slot >> 5;
+        const int qi = bk.get(SD, F_Q, j);
+        if (own) part_cxl += (mQ < qi) ? mQ : qi;              // G14
+        bk.put_if(own, SD, F_Q, j, qi - mQ);                   // Q <= 0 -> empty
         if (bslot[SD] == slot) bslot[SD] = BEST_INVALID;
         if constexpr (!BK::kRegs) __syncwarp();
     }
@@ -347,12 +385,11 @@ struct Engine {
             if (OWN == BID ? (Pa < Ps) : (Pa > Ps)) break;          // prices do not overlap
             const int ol = s & 31;
             const bool own = lane == ol;
+            const int sj = s >> 5;
             int Qs, myoid;
             if constexpr (BK::kRegs) {   // the owner's registers; Q broadcast by shuffle
-                int myq = 0;
-                myoid = 0;
-                bk.row(s >> 5, [&](auto J) { myq = bk.hot(OPP, F_Q, J); myoid = bk.hot(OPP, F_OID, J); });
-                Qs = __shfl_sync(FULL, myq, ol);
+                myoid = bk.get(OPP, F_OID, sj);
+                Qs = __shfl_sync(FULL, bk.get(OPP, F_Q, sj), ol);
             } else {                     // shared memory: every lane reads the slot
                 Qs = bk.ld(OPP, F_Q, s);
                 myoid = bk.ld(OPP, F_OID, s);
@@ -370,9 +407,7 @@ struct Engine {
                 part_trd += q;
             }
             ++ntr;                                                    // fills this call (logged = min(ntr, Tcap))
-            bk.row(s >> 5, [&](auto J) {
-                if (own) bk.set_hot(OPP, F_Q, J, Qs2);               // filled order removed (G10)
-            });
+            bk.put_if(own, OPP, F_Q, sj, Qs2);                      // filled order removed (G10)
             if (Qs2 == 0) bslot[OPP] = BEST_INVALID;
             if constexpr (!BK::kRegs) __syncwarp();
         }
@@ -396,23 +431,21 @@ struct Engine {
             }
         });
         // every lane stores the same value, so each lane later reads its own write
-        bk.st(OWN, F_TID, slot, mTID);
-        bk.st(OWN, F_TS, slot, mTS);
-        bk.st(OWN, F_TNS, slot, mTNS);
+        bk.put_cold(OWN, slot, mTID, mTS, mTNS);
         if constexpr (!BK::kRegs) __syncwarp();
         note_add<OWN>(slot, mP, mTS, mTNS);
     }
 
     __device__ __forceinline__ void message(const int4 a, const int4 b) {
         const int T = a.x, S = a.y, Q = a.z, P = a.w;
-        if (T == 0) return;                                          // padding (G21)
-        // T in 1..4 and S in {-1, +1}, else malformed (G22)
-        if (!(((unsigned)(T - 1) < 4u) & ((((unsigned)(S + 1)) & ~2u) == 0u))) {
-            if (lane == 0) count(ST_BAD, 1);
+        // T in 1..4 and S in {-1, +1}; T = 0 is padding (G21), anything else malformed (G22)
+        const unsigned t1 = (unsigned)(T - 1);
+        if (!((t1 < 4u) & ((((unsigned)(S + 1)) & ~2u) == 0u))) {
+            if (T != 0 && lane == 0) count(ST_BAD, 1);
             return;
         }
         // the paper's 8 (type x side) cases; cancel and delete share one
-        if ((unsigned)(T - 2) < 2u) {
+        if (t1 - 1u < 2u) {
             if (S == 1) cancel<BID>(Q, P, b.x);
             else cancel<ASK>(Q, P, b.x);
         } else {
@@ -422,9 +455,46 @@ struct Engine {
     }
 
     // L2 (G23): k-th best distinct price per side and its summed quantity;
-    // lane k keeps level k.  Absent levels are (-1, 0).
+    // lane k keeps level k.  Absent levels are (-1, 0).  Each level takes the
+    // warp minimum of the remaining keys and retires every slot at that price.
     template <int SD>
     __device__ __forceinline__ void l2_side(int L, int &outp, int &outq) const {
+        if constexpr (!BK::kRegs) {
+            l2_side_scan<SD>(L, outp, outq);
+            return;
+        }
+        outp = -1; outq = 0;
+        int key[KPL];
+        bool any = false;
+#pragma unroll UNR
+        for (int j = 0; j < KPL; ++j) {
+            const int p = bk.hot(SD, F_P, j);
+            const bool occ = bk.hot(SD, F_Q, j) > 0;
+            key[j] = occ ? ((SD == ASK) ? p : ~p) : INT_MAX;
+            any |= occ;
+        }
+        unsigned live = __ballot_sync(FULL, any);
+        for (int k = 0; k < L && live; ++k) {
+            int lk = key[0];
+#pragma unroll UNR
+            for (int j = 1; j < KPL; ++j) lk = min(lk, key[j]);
+            const int m = __reduce_min_sync(FULL, lk);
+            unsigned lq = 0;
+            bool left = false;
+#pragma unroll UNR
+            for (int j = 0; j < KPL; ++j) {
+                const bool hit = key[j] == m;
+                if (hit) { lq += (unsigned)bk.hot(SD, F_Q, j); key[j] = INT_MAX; }
+                left |= key[j] != INT_MAX;
+            }
+            const unsigned qs = __reduce_add_sync(FULL, lq);
+            if (lane == k) { outp = (SD == ASK) ? m : ~m; outq = (int)qs; }
+            live = __ballot_sync(FULL, left);
+        }
+    }
+    // shared-memory books: rescan with a "strictly worse than the previous level" filter
+    template <int SD>
+    __device__ __forceinline__ void l2_side_scan(int L, int &outp, int &outq) const {
         outp = -1; outq = 0;
         int prev = 0;
         bool have_prev = false;
@@ -506,15 +576,18 @@ __device__ __forceinline__ void run_books(const Params &p, BK &bk, int32_t *stag
             const uint32_t seq = chunk_seq + c, slot = seq & 1;
             mbar_wait(&bars[slot], (seq >> 1) & 1);
             uint32_t maddr = stage_u32 + slot * CH * 32;
-            const int cnt = min(CH, nmsg - c * CH);
-            for (int i = 0; i < cnt; ++i, maddr += 32) {
-                int4 a, bb;
-                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(maddr));
-                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4+16];"
-                             : "=r"(bb.x), "=r"(bb.y), "=r"(bb.z), "=r"(bb.w) : "r"(maddr));
-                e.message(a, bb);
-                if (--left == 0) {                     // end of a step: L2 snapshot (G23)
+            int cnt = min(CH, nmsg - c * CH);
+            while (cnt > 0) {                          // runs up to the next chunk or step end
+                const int run = min(cnt, left);
+                const uint32_t mend = maddr + 32u * run;
+                do {
+                    const int4 a = lds128(maddr), bb = lds128(maddr + 16);
+                    e.message(a, bb);
+                    maddr += 32;
+                } while (maddr != mend);
+                cnt -= run;
+                left -= run;
+                if (left == 0) {                       // end of a step: L2 snapshot (G23)
                     left = p.M;
                     if (p.l2out) e.l2_write(p.l2out + (((size_t)lb * p.n_steps + step) * p.L) * 4, p.L);
                     ++step;
