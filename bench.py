@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU owns the config's books; strong: the config's books are split")
     return ap.parse_args()
 
 
@@ -128,7 +130,9 @@ def run_reference(args):
     import oracle
     cfg = lobgen.CONFIGS[args.config]
     cores = len(os.sched_getaffinity(0))
-    nb = 2048  # bounded sample per step
+    # the oracle needs ~1 s per step for the whole C4 batch on a 16-core host, so each
+    # step is the full single-GPU workload; larger configs are capped to keep the run short
+    nb = min(cfg.n_books, 65536)
     msgs, init = lobgen.generate(cfg, n_books=nb)
     o = oracle.OracleBatch(nb, cfg.capacity, cfg.trades_cap, cfg.l2_levels, threads=cores)
 
@@ -144,7 +148,8 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     n = nb * cfg.n_msgs * args.steps
     v = n / dt
-    sample = f"first {nb} books of {cfg.name} ({nb * cfg.n_msgs} messages) per step, {args.steps} steps"
+    sample = (f"{nb} of {cfg.n_books} books of {cfg.name} ({nb * cfg.n_msgs} messages) per step, "
+              f"{args.steps} steps, {cores} threads over books")
     line = {"impl": "reference", "metric": "messages/sec", "value": v, "unit": "msg/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
@@ -192,6 +197,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2308_13289_b200 import LobBatch, launch_count
+    from paper_2308_13289_b200.shard import gather_rows, reduce_max, reduce_sum, shard_books
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -200,14 +206,15 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = lobgen.CONFIGS[args.config]
-    K = cfg.n_books
+    book0, K = shard_books(rank, world, cfg.n_books, args.scaling)
+    cfg = cfg.with_(n_books=K)
     S, M, L = cfg.n_steps, cfg.msgs_per_step, cfg.l2_levels
 
     # inputs: generated on the host (seeded by GLOBAL book id), pinned, then resident in HBM
     msgs_h = torch.empty((K, cfg.n_msgs, 8), dtype=torch.int32).pin_memory()
     init_h = torch.empty((K, cfg.init_levels, 4), dtype=torch.int32).pin_memory()
     t0 = time.time()
-    lobgen.generate(cfg, book_begin=rank * K, msgs_out=msgs_h.numpy(), init_out=init_h.numpy())
+    lobgen.generate(cfg, book_begin=book0, msgs_out=msgs_h.numpy(), init_out=init_h.numpy())
     gen_s = time.time() - t0
     msgs_d = msgs_h.to(dev)
     init_d = init_h.to(dev)
@@ -242,29 +249,19 @@ def main():
     n_launch = launch_count() - n_launch0
     if world > 1:
         dist.barrier()
-    elapsed_ms = start.elapsed_time(end)
+    elapsed_ms = reduce_max(start.elapsed_time(end), dev)       # the slowest rank's device time
     kernel_ms = [a.elapsed_time(z) for a, z in kev]
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t.item())
 
     # per-book counters and the trade counts of the last step (algorithmic bytes)
     st = b.stats()
     _, ntr = b.trades()
     trades_logged = int(ntr.sum().item())
-    if world > 1:
-        allst = torch.empty((world * K, st.shape[1]), dtype=st.dtype, device=dev)
-        dist.all_gather_into_tensor(allst, st)
-        tot = torch.tensor([trades_logged], dtype=torch.int64, device=dev)
-        dist.all_reduce(tot)
-        trades_total = int(tot.item())
-    else:
-        allst = st
-        trades_total = trades_logged
+    allst = gather_rows(st)                                     # NCCL gather of per-book counters
+    trades_total = reduce_sum(trades_logged, dev)
     stats_sum = allst.sum(0).cpu().tolist()
+    total_books = reduce_sum(K, dev)
 
-    total_msgs = world * K * cfg.n_msgs * args.steps
+    total_msgs = total_books * cfg.n_msgs * args.steps
     value = total_msgs / (elapsed_ms / 1e3)
     ms_per_step = elapsed_ms / args.steps
 
@@ -312,10 +309,8 @@ def main():
             e2e_step()
         e_e.record(stream)
         torch.cuda.synchronize()
-        et = torch.tensor([e_s.elapsed_time(e_e)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e_v = world * K * cfg.n_msgs * args.e2e_steps / (float(et.item()) / 1e3)
+        et = reduce_max(e_s.elapsed_time(e_e), dev)
+        e2e_v = total_books * cfg.n_msgs * args.e2e_steps / (et / 1e3)
         e2e = {"value": e2e_v, "unit": "msg/s",
                "h2d_bytes_per_step": msgs_h.numel() * 4 + init_h.numel() * 4,
                "d2h_bytes_per_step": h_l2.numel() * 4 + h_st.numel() * 8,
@@ -329,9 +324,9 @@ def main():
     if rank == 0:
         line = {"metric": "messages/sec", "value": value, "unit": "msg/s", "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "int32", "data": "synthetic",
                 "ns_per_message": 1e9 / value, "ns_per_message_per_gpu": 1e9 / value * world,
-                "config": {"workload": workload_desc(cfg, K), "books_per_gpu": K, "books_total": world * K,
+                "config": {"workload": workload_desc(cfg, K), "books_per_gpu": K, "books_total": total_books,
                            "capacity": cfg.capacity, "msgs_per_book": cfg.n_msgs, "n_steps": S,
                            "msgs_per_step": M, "l2_levels": L, "trades_cap": cfg.trades_cap,
                            "profile": cfg.profile, "seed": cfg.seed, "parallelism": f"books sharded x{world}",
