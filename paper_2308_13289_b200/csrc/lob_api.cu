@@ -30,15 +30,18 @@ int cuda_fail(cudaError_t e, const char *where) {
     return LOB_ECUDA;
 }
 
-constexpr int REG_WARPS = 4;  // warps (books) per CTA on the register path
-
-// slots per lane: 1..4 registers, 8/16/32/64 shared memory
-int kpl_bucket(int N) {
-    int k = (N + 31) / 32;
-    if (k <= 4) return k;
-    int b = 8;
-    while (b < k) b <<= 1;
-    return b;
+// Book geometry: KPL register rows per thread and side, W warps per book.
+//   N <= 128: KPL = ceil(N/32), W = 1 (4 books per CTA)
+//   N <= 256: KPL = 8, W = 1;  above: KPL = 8, W = 2/4/8 (one book per CTA)
+struct Geo {
+    int kpl, w;
+};
+Geo geo_of(int N) {
+    if (N <= 128) return {(N + 31) / 32, 1};
+    if (N <= 256) return {8, 1};
+    int w = 2;
+    while (256 * w < N) w <<= 1;
+    return {8, w};
 }
 
 struct Layout {
@@ -51,7 +54,8 @@ bool layout_of(const lob_config *c, Layout *L) {
         c->l2_levels < 1 || c->l2_levels > LOB_MAX_L2_LEVELS)
         return false;
     const size_t K = (size_t)c->n_books;
-    L->NP = 32 * kpl_bucket(c->capacity);
+    const Geo g = geo_of(c->capacity);
+    L->NP = 32 * g.kpl * g.w;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     L->off_book = 0;
     L->off_trades = al(L->off_book + K * 2 * NF * L->NP * sizeof(int32_t));
@@ -67,9 +71,8 @@ struct lob_ctx {
     Layout lay;
     char *state;
     int sm_count;
-    int kpl;
+    Geo geo;
     int grid_cap;  // persistent grid: resident CTAs for the step kernel
-    size_t smem_bytes;
     int32_t *book() const { return reinterpret_cast<int32_t *>(state + lay.off_book); }
     int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
     int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
@@ -77,17 +80,23 @@ struct lob_ctx {
 };
 
 namespace {
+// call f(IC<KPL>, IC<W>, IC<G>) for the compiled geometry (G = books per CTA)
 template <class F>
-void for_kpl(int kpl, F &&f) {
-    switch (kpl) {
-        case 1: f(std::integral_constant<int, 1>()); break;
-        case 2: f(std::integral_constant<int, 2>()); break;
-        case 3: f(std::integral_constant<int, 3>()); break;
-        case 4: f(std::integral_constant<int, 4>()); break;
-        case 8: f(std::integral_constant<int, 8>()); break;
-        case 16: f(std::integral_constant<int, 16>()); break;
-        case 32: f(std::integral_constant<int, 32>()); break;
-        default: f(std::integral_constant<int, 64>()); break;
+void for_geo(Geo g, F &&f) {
+    if (g.w == 1) {
+        switch (g.kpl) {
+            case 1: f(IC<1>(), IC<1>(), IC<4>()); break;
+            case 2: f(IC<2>(), IC<1>(), IC<4>()); break;
+            case 3: f(IC<3>(), IC<1>(), IC<4>()); break;
+            case 4: f(IC<4>(), IC<1>(), IC<4>()); break;
+            default: f(IC<8>(), IC<1>(), IC<4>()); break;
+        }
+    } else {
+        switch (g.w) {
+            case 2: f(IC<8>(), IC<2>(), IC<1>()); break;
+            case 4: f(IC<8>(), IC<4>(), IC<1>()); break;
+            default: f(IC<8>(), IC<8>(), IC<1>()); break;
+        }
     }
 }
 
@@ -117,16 +126,11 @@ int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M,
     p.N = ctx->cfg.capacity; p.NP = ctx->lay.NP; p.Tcap = ctx->cfg.trades_cap; p.L = ctx->cfg.l2_levels;
     p.n_steps = n_steps; p.M = M; p.book0 = book0; p.nb = nb;
     int rc = LOB_OK;
-    for_kpl(ctx->kpl, [&](auto kc) {
-        constexpr int KPL = decltype(kc)::value;
-        if constexpr (KPL <= 4) {
-            const unsigned need = blocks_for(nb, REG_WARPS);
-            const unsigned grid = need < (unsigned)ctx->grid_cap ? need : (unsigned)ctx->grid_cap;
-            lob_step_reg<KPL, REG_WARPS><<<grid, REG_WARPS * 32, 0, st>>>(p);
-        } else {
-            const unsigned grid = (unsigned)nb < (unsigned)ctx->grid_cap ? (unsigned)nb : (unsigned)ctx->grid_cap;
-            lob_step_smem<KPL><<<grid, 32, ctx->smem_bytes, st>>>(p);
-        }
+    for_geo(ctx->geo, [&](auto kc, auto wc, auto gc) {
+        constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, G = decltype(gc)::value;
+        const unsigned need = blocks_for(nb, G);
+        const unsigned grid = need < (unsigned)ctx->grid_cap ? need : (unsigned)ctx->grid_cap;
+        lob_step<KPL, W, G><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p);
         rc = after_launch("lob_step kernel");
     });
     return rc;
@@ -161,25 +165,19 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
     c->lay = L;
     c->state = static_cast<char *>(d_state);
     c->sm_count = sms;
-    c->kpl = kpl_bucket(cfg->capacity);
+    c->geo = geo_of(cfg->capacity);
     int per_sm = 1;
     int rc = LOB_OK;
-    for_kpl(c->kpl, [&](auto kc) {
-        constexpr int KPL = decltype(kc)::value;
-        if constexpr (KPL <= 4) {
-            c->smem_bytes = 0;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step_reg<KPL, REG_WARPS>, REG_WARPS * 32, 0);
-        } else {
-            c->smem_bytes = smem_step_bytes(KPL);
-            e = cudaFuncSetAttribute(lob_step_smem<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)c->smem_bytes);
-            if (e == cudaSuccess)
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step_smem<KPL>, 32, c->smem_bytes);
-        }
-        if (e == cudaSuccess && KPL * 32 * 2 * NF * 4 > 48 * 1024)
-            e = cudaFuncSetAttribute(lob_export_l2<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     KPL * 32 * 2 * NF * 4);
-        if (e != cudaSuccess) rc = cuda_fail(e, "occupancy query");
+    for_geo(c->geo, [&](auto kc, auto wc, auto gc) {
+        constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, G = decltype(gc)::value;
+        constexpr int smem = step_smem_bytes<KPL, W, G>();
+        e = cudaFuncSetAttribute(lob_step<KPL, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step<KPL, W, G>, 32 * W * G, smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(lob_export_l2<KPL, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     export_l2_smem_bytes<KPL, W>());
+        if (e != cudaSuccess) rc = cuda_fail(e, "kernel attribute / occupancy query");
     });
     if (rc != LOB_OK) { delete c; return rc; }
     c->grid_cap = sms * (per_sm > 0 ? per_sm : 1);
@@ -295,10 +293,10 @@ int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *stream) {
     const int K = ctx->cfg.n_books;
     if (K == 0) return LOB_OK;
     if (!d_out || reinterpret_cast<uintptr_t>(d_out) % 16) return fail(LOB_EINVAL, "d_out null or misaligned%s");
-    for_kpl(ctx->kpl, [&](auto kc) {
-        constexpr int KPL = decltype(kc)::value;
-        lob_export_l2<KPL><<<K, 32, KPL * 32 * 2 * NF * 4, (cudaStream_t)stream>>>(
-            ctx->book(), d_out, K, ctx->cfg.capacity, ctx->lay.NP, ctx->cfg.l2_levels);
+    for_geo(ctx->geo, [&](auto kc, auto wc, auto) {
+        constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value;
+        lob_export_l2<KPL, W><<<K, 32 * W, export_l2_smem_bytes<KPL, W>(), (cudaStream_t)stream>>>(
+            ctx->book(), d_out, K, ctx->cfg.capacity, ctx->cfg.l2_levels);
         rc = after_launch("lob_export_l2");
     });
     return rc;
