@@ -46,7 +46,7 @@ Geo geo_of(int N) {
 
 struct Layout {
     int NP;
-    size_t off_book, off_trades, off_ntr, off_stats, total;
+    size_t off_book, off_trades, off_ntr, off_stats, off_sched, total;
 };
 
 bool layout_of(const lob_config *c, Layout *L) {
@@ -61,7 +61,8 @@ bool layout_of(const lob_config *c, Layout *L) {
     L->off_trades = al(L->off_book + K * 2 * NF * L->NP * sizeof(int32_t));
     L->off_ntr = al(L->off_trades + K * (size_t)c->trades_cap * 6 * sizeof(int32_t));
     L->off_stats = al(L->off_ntr + K * sizeof(int32_t));
-    L->total = al(L->off_stats + K * NST * sizeof(long long));
+    L->off_sched = al(L->off_stats + K * NST * sizeof(long long));
+    L->total = al(L->off_sched + 2 * sizeof(unsigned));
     return true;
 }
 }  // namespace
@@ -77,6 +78,7 @@ struct lob_ctx {
     int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
     int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
     long long *stats() const { return reinterpret_cast<long long *>(state + lay.off_stats); }
+    unsigned *sched() const { return reinterpret_cast<unsigned *>(state + lay.off_sched); }
 };
 
 namespace {
@@ -122,7 +124,7 @@ int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M,
     if (nb <= 0) return LOB_OK;
     Params p;
     p.book = ctx->book(); p.trades = ctx->trades(); p.ntrades = ctx->ntr(); p.stats = ctx->stats();
-    p.msgs = d_msgs; p.l2out = d_l2;
+    p.msgs = d_msgs; p.l2out = d_l2; p.sched = ctx->sched();
     p.N = ctx->cfg.capacity; p.NP = ctx->lay.NP; p.Tcap = ctx->cfg.trades_cap; p.L = ctx->cfg.l2_levels;
     p.n_steps = n_steps; p.M = M; p.book0 = book0; p.nb = nb;
     int rc = LOB_OK;
@@ -197,7 +199,8 @@ int lob_init(lob_ctx *ctx, const int32_t *d_init_l2, int32_t init_levels, int32_
     if (K == 0) return LOB_OK;
     const int wpb = 8;
     lob_init_kernel<<<blocks_for(K, wpb), wpb * 32, 0, (cudaStream_t)stream>>>(
-        ctx->book(), ctx->trades(), ctx->ntr(), ctx->stats(), K, ctx->cfg.capacity, ctx->lay.NP, ctx->cfg.trades_cap,
+        ctx->book(), ctx->trades(), ctx->ntr(), ctx->stats(), ctx->sched(), K, ctx->cfg.capacity, ctx->lay.NP,
+        ctx->cfg.trades_cap,
         d_init_l2, init_levels, init_ts, init_tns);
     return after_launch("lob_init_kernel");
 }

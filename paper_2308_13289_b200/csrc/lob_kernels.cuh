@@ -54,6 +54,7 @@ struct Params {
     long long *stats;      // [K][NST]
     const int32_t *msgs;   // [nb][n_steps*M][8]  (relative to book0)
     int32_t *l2out;        // [nb][n_steps][L][4] or null (relative to book0)
+    unsigned *sched;       // [2]: next book, finished groups (zero between launches)
     int N, NP, Tcap, L, n_steps, M;
     int book0, nb;         // books [book0, book0+nb) of the state
 };
@@ -213,20 +214,22 @@ template <class BK>
 struct Engine {
     static constexpr int KPL = BK::KPL, W = BK::W, GT = BK::GT;
     BK bk;
-    int tid, N, Tcap, ntr;
-    int32_t *tlog;          // this book's trade log [Tcap][6]
+    const Params &p;
+    int tid, book, ntr;
     uint32_t sc;            // shared: counters [NST] int64 (thread 0 only), best times bt[2][2] int32,
-                            //         then (W > 1) the cross-warp exchange buffers xb[2][W] u32
+                            //         cross-warp exchange xb[2][W] u32, next-book word
     int xph;                // exchange buffer phase (uniform)
     // uniform best-order cache per side (Eq.5 + G1/G4): slot or BEST_*, and its price
     int bslot[2], bP[2];
     long long part_cxl;     // cancelled quantity, accumulated on the owner thread (G14)
     long long part_trd;     // traded quantity, accumulated on the owner thread
 
+    __device__ __forceinline__ Engine(const Params &p_) : p(p_) {}
+
     __device__ __forceinline__ void count(int c, long long x) {  // thread 0 only
         sts64(sc + 8u * c, lds64(sc + 8u * c) + x);
     }
-    __device__ __forceinline__ bool valid(int j) const { return j < KPL - 1 || j * GT + tid < N; }
+    __device__ __forceinline__ bool valid(int j) const { return j < KPL - 1 || j * GT + tid < p.N; }
     __device__ __forceinline__ uint32_t bt_addr(int sd, int k) const { return sc + 8u * NST + 4u * (2 * sd + k); }
 
     // ---- group reductions: warp REDUX, then (W > 1) one exchange through shared memory
@@ -392,8 +395,8 @@ struct Engine {
             const int q = Qs - Qs2;                                  // Q_j = Q_s - Q_s'
             Qa = Qa - Qs;                                            // Q_a' = Q_a - Q_s
             if (own) {
-                if (ntr < Tcap) {                                    // Eq.3 record, Eq.4 cap (G8)
-                    int2 *t = reinterpret_cast<int2 *>(tlog + (size_t)ntr * 6);
+                if (ntr < p.Tcap) {                                  // Eq.3 record, Eq.4 cap (G8)
+                    int2 *t = reinterpret_cast<int2 *>(p.trades + ((size_t)book * p.Tcap + ntr) * 6);
                     t[0] = make_int2(Ps, q);
                     t[1] = make_int2(mOID, myoid);
                     t[2] = make_int2(mTS, mTNS);
@@ -491,7 +494,7 @@ struct Engine {
 // Per-book shared scratch: counters [NST] int64, best times [2][2] int32,
 // cross-warp exchange buffers [2][W] u32.
 template <int W>
-constexpr int scratch_bytes() { return 8 * NST + 16 + 8 * W; }
+constexpr int scratch_bytes() { return 8 * NST + 16 + 8 * W + 8; }
 
 // Dynamic shared memory of one CTA of G books of (KPL, W).
 template <int KPL, int W, int G>
@@ -501,7 +504,10 @@ constexpr int step_smem_bytes() {
 
 // Persistent: group g of CTA b walks books (b*G + g), + gridDim.x*G, ...
 template <int KPL, int W, int G>
-__global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 8 : (KPL <= 4 ? 6 : (W == 1 ? 4 : 1))))
+#ifndef MINB4
+#define MINB4 7
+#endif
+__global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : 1))))
     lob_step(const Params p) {
     using BK = RegBook<KPL, W>;
     extern __shared__ __align__(128) unsigned char dyn[];
@@ -522,7 +528,22 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 8 : (KPL <= 4 ? 6 : (W
     const int nmsg = p.n_steps * p.M;
     const int nchunks = (nmsg + CH - 1) / CH;
     uint32_t chunk_seq = 0;
-    for (int lb = blockIdx.x * G + g; lb < p.nb; lb += gridDim.x * G) {
+    // dynamic book scheduling: deep sweeps make books unequal, so a group takes
+    // the next book from a global counter (fetched one book ahead)
+    const uint32_t next_addr = scratch + 8u * NST + 16u + 8u * W;
+    int next = 0;
+    if (tid == 0) next = (int)atomicAdd(p.sched, 1u);
+    for (;;) {
+        int lb;
+        if constexpr (W == 1) {
+            lb = __shfl_sync(FULL, next, 0);
+        } else {
+            if (tid == 0) sts32(next_addr, next);
+            __syncthreads();
+            lb = lds32(next_addr);
+        }
+        if (lb >= p.nb) break;
+        if (tid == 0) next = (int)atomicAdd(p.sched, 1u);
         const int b = p.book0 + lb;
         const int4 *src = reinterpret_cast<const int4 *>(p.msgs + (size_t)lb * nmsg * 8);
         // prologue: the first two chunks are in flight before the book is loaded
@@ -540,15 +561,14 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 8 : (KPL <= 4 ? 6 : (W
             }
         }
         if (tid < NST) sts64(scratch + 8u * tid, 0);
-        Engine<BK> e;
+        Engine<BK> e(p);
         e.bk.cold = cold;
         e.bk.tid = tid;
+        e.tid = tid; e.book = b; e.ntr = 0; e.sc = scratch; e.xph = 0;
+        e.part_cxl = 0; e.part_trd = 0;
         e.bk.load(p.book + (size_t)b * 2 * NF * BK::NP);
-        e.tid = tid; e.N = p.N; e.Tcap = p.Tcap; e.ntr = 0; e.sc = scratch; e.xph = 0;
-        e.tlog = p.trades + (size_t)b * p.Tcap * 6;
         e.bslot[0] = e.bslot[1] = BEST_INVALID;
         e.bP[0] = e.bP[1] = 0;
-        e.part_cxl = 0; e.part_trd = 0;
         int left = p.M, step = 0;
         for (int c = 0; c < nchunks; ++c) {
             const uint32_t seq = chunk_seq + c, slot = seq & 1;
@@ -606,15 +626,24 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 8 : (KPL <= 4 ? 6 : (W
         }
         if (tid == 0) p.ntrades[b] = logged;
     }
+    // the last group to finish re-arms the counters for the next launch
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(p.sched + 1, 1u) == gridDim.x * G - 1) {
+            atomicExch(p.sched, 0u);
+            atomicExch(p.sched + 1, 0u);
+        }
+    }
 }
 
 // ------------------------------------------------------------- init / exports
 // a0: -1 everywhere, counters 0, then one synthetic order per
 // populated L2 level (G24).  One warp per book.
-__global__ void lob_init_kernel(int32_t *book, int32_t *trades, int32_t *ntrades, long long *stats, int K, int N,
-                                int NP, int Tcap, const int32_t *init_l2, int L0, int ts, int tns) {
+__global__ void lob_init_kernel(int32_t *book, int32_t *trades, int32_t *ntrades, long long *stats, unsigned *sched,
+                                int K, int N, int NP, int Tcap, const int32_t *init_l2, int L0, int ts, int tns) {
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (blockIdx.x == 0 && threadIdx.x < 2) sched[threadIdx.x] = 0u;
     if (b >= K) return;
     int32_t *bb = book + (size_t)b * 2 * NF * NP;
     for (int i = lane; i < 2 * NF * NP; i += 32) bb[i] = -1;
@@ -679,8 +708,10 @@ __global__ void __launch_bounds__(32 * W) lob_export_l2(const int32_t *book, int
     extern __shared__ __align__(128) unsigned char dyn[];
     const int b = blockIdx.x;
     if (b >= K) return;
-    Engine<BK> e;
-    e.tid = threadIdx.x; e.N = N; e.xph = 0;
+    Params p{};
+    p.N = N;
+    Engine<BK> e(p);
+    e.tid = threadIdx.x; e.xph = 0;
     e.bk.tid = threadIdx.x;
     e.bk.cold = smem_u32(dyn);
     e.sc = smem_u32(dyn + 2 * BK::NP * 16);
