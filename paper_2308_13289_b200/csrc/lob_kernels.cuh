@@ -507,7 +507,7 @@ template <int KPL, int W, int G>
 #ifndef MINB4
 #define MINB4 7
 #endif
-__global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : 1))))
+__global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : 16 / W))))
     lob_step(const Params p) {
     using BK = RegBook<KPL, W>;
     extern __shared__ __align__(128) unsigned char dyn[];
@@ -528,22 +528,12 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
     const int nmsg = p.n_steps * p.M;
     const int nchunks = (nmsg + CH - 1) / CH;
     uint32_t chunk_seq = 0;
-    // dynamic book scheduling: deep sweeps make books unequal, so a group takes
-    // the next book from a global counter (fetched one book ahead)
+    // dynamic book scheduling: deep sweeps make books unequal, so after its first
+    // (static) book a group takes the next one from a global counter when it is free
     const uint32_t next_addr = scratch + 8u * NST + 16u + 8u * W;
-    int next = 0;
-    if (tid == 0) next = (int)atomicAdd(p.sched, 1u);
-    for (;;) {
-        int lb;
-        if constexpr (W == 1) {
-            lb = __shfl_sync(FULL, next, 0);
-        } else {
-            if (tid == 0) sts32(next_addr, next);
-            __syncthreads();
-            lb = lds32(next_addr);
-        }
-        if (lb >= p.nb) break;
-        if (tid == 0) next = (int)atomicAdd(p.sched, 1u);
+    const int groups = gridDim.x * G;
+    int lb = blockIdx.x * G + g;
+    while (lb < p.nb) {
         const int b = p.book0 + lb;
         const int4 *src = reinterpret_cast<const int4 *>(p.msgs + (size_t)lb * nmsg * 8);
         // prologue: the first two chunks are in flight before the book is loaded
@@ -625,6 +615,15 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
             p.stats[(size_t)b * NST + tid] += v;
         }
         if (tid == 0) p.ntrades[b] = logged;
+        int next = 0;
+        if (tid == 0) next = groups + (int)atomicAdd(p.sched, 1u);
+        if constexpr (W == 1) {
+            lb = __shfl_sync(FULL, next, 0);
+        } else {
+            if (tid == 0) sts32(next_addr, next);
+            __syncthreads();
+            lb = lds32(next_addr);
+        }
     }
     // the last group to finish re-arms the counters for the next launch
     if (tid == 0) {
