@@ -55,6 +55,8 @@ def _load():
             lib.oracle_init.argtypes = [P, i32, i32, P, i32, i32, i32]
             lib.oracle_process.restype = ctypes.c_int
             lib.oracle_process.argtypes = [P, i32, i32, P, i32, i32, P]
+            lib.oracle_process_ex.restype = ctypes.c_int
+            lib.oracle_process_ex.argtypes = [P, i32, i32, P, i32, i32, P, P]
             for name in ("oracle_get_book", "oracle_get_l2", "oracle_get_stats",
                          "oracle_get_violations"):
                 getattr(lib, name).argtypes = [P, P]
@@ -102,18 +104,23 @@ class OracleBatch:
         if rc != 0:
             raise ValueError("oracle_init: init_levels must be <= capacity")
 
-    def process(self, msgs: np.ndarray, n_steps: int, msgs_per_step: int, l2: bool = True):
+    def process(self, msgs: np.ndarray, n_steps: int, msgs_per_step: int, l2: bool = True,
+                l1: bool = False):
+        """Returns the per-step L2 [K][S][L][4] (or None); with l1=True returns
+        (l2, l1) where l1 is the per-message Level-1 trace [K][S*M][4] (NEXT row N1)."""
         msgs = np.ascontiguousarray(msgs, dtype=np.int32)
         assert msgs.shape == (self.K, n_steps * msgs_per_step, 8), msgs.shape
         out = np.empty((self.K, n_steps, self.L, 4), np.int32) if l2 else None
+        l1o = np.empty((self.K, n_steps * msgs_per_step, 4), np.int32) if l1 else None
         if self.threads == 1 or self.K <= 1:
-            self.lib.oracle_process(self.ctx, 0, self.K, _ptr(msgs), n_steps, msgs_per_step, _ptr(out))
+            self.lib.oracle_process_ex(self.ctx, 0, self.K, _ptr(msgs), n_steps, msgs_per_step, _ptr(out),
+                                       _ptr(l1o))
         else:
             with ThreadPoolExecutor(self.threads) as ex:   # ctypes releases the GIL
-                list(ex.map(lambda r: self.lib.oracle_process(
-                    self.ctx, r[0], r[1], _ptr(msgs), n_steps, msgs_per_step, _ptr(out)),
+                list(ex.map(lambda r: self.lib.oracle_process_ex(
+                    self.ctx, r[0], r[1], _ptr(msgs), n_steps, msgs_per_step, _ptr(out), _ptr(l1o)),
                     self._ranges()))
-        return out
+        return (out, l1o) if l1 else out
 
     def book(self) -> np.ndarray:
         out = np.empty((self.K, 2, self.N, 6), np.int32)

@@ -291,8 +291,8 @@ static void process(oracle_ctx *X, obook *b, const int32_t *m) {
 /* L2 top-L (G23): k-th best distinct price per side with its summed quantity;
  * absent levels are (-1, 0).  The sum is taken in int64 and reported as its
  * low 32 bits (two's complement); generator profiles keep it < 2^31 (G20). */
-static void l2_snapshot(oracle_ctx *X, const obook *b, int32_t *out /*[L][4]*/) {
-    int N = X->N, L = X->L;
+static void l2_levels(oracle_ctx *X, const obook *b, int32_t *out /*[L][4]*/, int L) {
+    int N = X->N;
     for (int s = 0; s < 2; s++) {
         const int32_t *side = s ? b->B : b->A;
         int is_ask = (s == 0);
@@ -326,6 +326,13 @@ static void l2_snapshot(oracle_ctx *X, const obook *b, int32_t *out /*[L][4]*/) 
         }
     }
 }
+
+static void l2_snapshot(oracle_ctx *X, const obook *b, int32_t *out /*[L][4]*/) { l2_levels(X, b, out, X->L); }
+
+/* NEXT row N1: Level-1 data after every processed message:
+ * [best ask P, volume at it, best bid P, volume at it] = level 1 of the L2
+ * definition (G23), absent side (-1, 0). */
+static void l1_snapshot(oracle_ctx *X, const obook *b, int32_t *out /*[4]*/) { l2_levels(X, b, out, 1); }
 
 /* ------------------------------------------------------------ public API */
 
@@ -395,8 +402,8 @@ int oracle_init(oracle_ctx *X, int32_t k0, int32_t k1, const int32_t *init_l2, i
 /* One call over books [k0, k1): the trade log is cleared at the start of the
  * call (G9); counters accumulate; L2 after the last message of each step.
  * msgs: [K][n_steps*M][8]; l2_out: [K][n_steps][L][4] or NULL. */
-int oracle_process(oracle_ctx *X, int32_t k0, int32_t k1, const int32_t *msgs, int32_t n_steps,
-                   int32_t M, int32_t *l2_out) {
+int oracle_process_ex(oracle_ctx *X, int32_t k0, int32_t k1, const int32_t *msgs, int32_t n_steps,
+                      int32_t M, int32_t *l2_out, int32_t *l1_out /* [K][n_steps*M][4] or NULL */) {
     int64_t per_book = (int64_t)n_steps * M;
     for (int k = k0; k < k1; k++) {
         obook *b = &X->books[k];
@@ -404,11 +411,19 @@ int oracle_process(oracle_ctx *X, int32_t k0, int32_t k1, const int32_t *msgs, i
         b->n_trades = 0;
         const int32_t *mk = msgs + (size_t)k * per_book * M_NF;
         for (int s = 0; s < n_steps; s++) {
-            for (int i = 0; i < M; i++) process(X, b, mk + ((size_t)s * M + i) * M_NF);
+            for (int i = 0; i < M; i++) {
+                process(X, b, mk + ((size_t)s * M + i) * M_NF);
+                if (l1_out) l1_snapshot(X, b, l1_out + ((size_t)k * per_book + (size_t)s * M + i) * 4);
+            }
             if (l2_out) l2_snapshot(X, b, l2_out + (((size_t)k * n_steps + s) * X->L) * 4);
         }
     }
     return 0;
+}
+
+int oracle_process(oracle_ctx *X, int32_t k0, int32_t k1, const int32_t *msgs, int32_t n_steps,
+                   int32_t M, int32_t *l2_out) {
+    return oracle_process_ex(X, k0, k1, msgs, n_steps, M, l2_out, NULL);
 }
 
 /* exports: book [K][2][N][6] (side 0 = asks), trades [K][T_cap][6] + counts,

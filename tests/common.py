@@ -64,7 +64,12 @@ def run_golden_case(make_engine, case):
         S, M = call["n_steps"], call["msgs_per_step"]
         msgs = _msgs(call)
         exp = call["expect"]
-        l2 = eng.process(msgs[None], S, M, l2=True)
+        if "l1_trace" in exp:
+            l2, l1 = eng.process(msgs[None], S, M, l2=True, l1=True)
+            np.testing.assert_array_equal(l1[0], np.asarray(exp["l1_trace"], np.int32),
+                                          err_msg=f"call {ci} L1 trace")
+        else:
+            l2 = eng.process(msgs[None], S, M, l2=True)
         if "trades" in exp:
             tr, cnt = eng.trades()
             want = np.full((T_cap, 6), -1, np.int32)

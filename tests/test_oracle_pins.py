@@ -248,3 +248,21 @@ def test_generator_is_shard_invariant():
     b, ib = lobgen.generate(cfg, book_begin=40, n_books=24, threads=1)
     np.testing.assert_array_equal(a[40:], b)
     np.testing.assert_array_equal(ia[40:], ib)
+
+
+# ------------------------------------------------- NEXT row N1: Level-1 trace
+@pytest.mark.parametrize("profile", ["lobster", "heavy_market", "cancel_heavy"])
+def test_l1_trace_equals_fifo_top_of_book(profile):
+    """Level-1 after every message equals the independent FIFO engine's
+    top of book after that message."""
+    cfg = lobgen.Config("l1", 12, 100, 4, 50, 20, 4000, 3, profile, 31)
+    msgs, init = lobgen.generate(cfg)
+    o = oracle.OracleBatch(12, 100, 4000, 3)
+    o.init(init, lobgen.INIT_TS, lobgen.INIT_TNS)
+    l2, l1 = o.process(msgs, cfg.n_steps, cfg.msgs_per_step, l1=True)
+    assert l1.shape == (12, cfg.n_msgs, 4)
+    for k in range(12):
+        _, snaps = run_stream(msgs[k], cfg.n_msgs, 1, 1, init[k], lobgen.INIT_TS, lobgen.INIT_TNS)
+        np.testing.assert_array_equal(l1[k], np.asarray(snaps, np.int32)[:, 0], err_msg=f"book {k}")
+        # consistency with the per-step L2 (level 1 at the step boundaries)
+        np.testing.assert_array_equal(l1[k, cfg.msgs_per_step - 1::cfg.msgs_per_step], l2[k, :, 0])
