@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--l1", action="store_true",
+                    help="also write the per-message Level-1 trace (NEXT row N1, lob_process_messages_l1)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every GPU owns the config's books; strong: the config's books are split")
     return ap.parse_args()
@@ -219,6 +221,7 @@ def main():
     msgs_d = msgs_h.to(dev)
     init_d = init_h.to(dev)
     l2_d = torch.empty((K, S, L, 4), dtype=torch.int32, device=dev)
+    l1_d = torch.empty((K, cfg.n_msgs, 4), dtype=torch.int32, device=dev) if args.l1 else None
     b = LobBatch(K, cfg.capacity, cfg.trades_cap, L, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -226,7 +229,7 @@ def main():
         b.init(init_d, lobgen.INIT_TS, lobgen.INIT_TNS)
         if evs is not None:
             evs[0].record(stream)
-        b.process(msgs_d, S, M, l2_out=l2_d)
+        b.process(msgs_d, S, M, l2_out=l2_d, l1=args.l1, l1_out=l1_d)
         if evs is not None:
             evs[1].record(stream)
 
@@ -268,7 +271,7 @@ def main():
     # roofline of the dominant kernel (lob_step): algorithmic bytes per launch
     book_bytes = 2 * K * 2 * cfg.capacity * LOGICAL_ORDER_BYTES     # state read + written once
     alg_bytes = (K * cfg.n_msgs * MSG_BYTES + trades_logged * TRADE_BYTES + K * S * L * L2_LEVEL_BYTES
-                 + book_bytes + 2 * K * STAT_BYTES)
+                 + book_bytes + 2 * K * STAT_BYTES + (K * cfg.n_msgs * L2_LEVEL_BYTES if args.l1 else 0))
     kmean_ms = statistics.mean(kernel_ms)
     peak, peak_src, _ = load_peaks()
     achieved = alg_bytes / (kmean_ms / 1e3) / 1e9
@@ -337,7 +340,8 @@ def main():
                 "totals": dict(zip(["msgs", "bad", "trades", "trades_dropped", "traded_qty", "cancelled_qty",
                                     "unknown_cancels", "add_overflow", "overflow_qty", "market_discarded_qty"],
                                    stats_sum)),
-                "trades_logged_last_step": trades_total, "generate_s": gen_s}
+                "trades_logged_last_step": trades_total, "generate_s": gen_s,
+                "l1_trace": bool(args.l1)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -104,6 +104,14 @@ int lob_init(lob_ctx *ctx, const int32_t *d_init_l2, int32_t init_levels, int32_
 int lob_process_messages(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps,
                          int32_t msgs_per_step, int32_t *d_l2_out, void *cuda_stream);
 
+/* NEXT row N1: lob_process_messages plus the Level-1 trace --
+ * after EVERY message, [best ask P, total Q at it, best bid P, total Q at it]
+ * (the exec-env state of P:L435-441; absent side (-1, 0)) into d_l1_out, a
+ * [K][n_steps*msgs_per_step][4] int32 buffer (required, 16-byte aligned).
+ * Everything else is identical to lob_process_messages. */
+int lob_process_messages_l1(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t msgs_per_step,
+                            int32_t *d_l2_out, int32_t *d_l1_out, void *cuda_stream);
+
 /* Same call with HOST buffers (end-to-end path): copies h_msgs (pinned host,
  * [K][n_steps*msgs_per_step][8]) into the caller's device buffer d_msgs_buf,
  * processes it, and copies the L2 snapshots (if h_l2_out is non-NULL; device

@@ -120,11 +120,11 @@ int after_launch(const char *what) {
 unsigned blocks_for(long long threads, int bs) { return (unsigned)((threads + bs - 1) / bs); }
 
 int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M, int32_t *d_l2, int book0, int nb,
-                cudaStream_t st) {
+                cudaStream_t st, int32_t *d_l1 = nullptr) {
     if (nb <= 0) return LOB_OK;
     Params p;
     p.book = ctx->book(); p.trades = ctx->trades(); p.ntrades = ctx->ntr(); p.stats = ctx->stats();
-    p.msgs = d_msgs; p.l2out = d_l2; p.sched = ctx->sched();
+    p.msgs = d_msgs; p.l2out = d_l2; p.l1out = d_l1; p.sched = ctx->sched();
     p.N = ctx->cfg.capacity; p.NP = ctx->lay.NP; p.Tcap = ctx->cfg.trades_cap; p.L = ctx->cfg.l2_levels;
     p.n_steps = n_steps; p.M = M; p.book0 = book0; p.nb = nb;
     int rc = LOB_OK;
@@ -132,7 +132,8 @@ int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M,
         constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, G = decltype(gc)::value;
         const unsigned need = blocks_for(nb, G);
         const unsigned grid = need < (unsigned)ctx->grid_cap ? need : (unsigned)ctx->grid_cap;
-        lob_step<KPL, W, G><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p);
+        if (d_l1) lob_step<KPL, W, G, true><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p);
+        else lob_step<KPL, W, G, false><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p);
         rc = after_launch("lob_step kernel");
     });
     return rc;
@@ -173,9 +174,11 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
     for_geo(c->geo, [&](auto kc, auto wc, auto gc) {
         constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, G = decltype(gc)::value;
         constexpr int smem = step_smem_bytes<KPL, W, G>();
-        e = cudaFuncSetAttribute(lob_step<KPL, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        e = cudaFuncSetAttribute(lob_step<KPL, W, G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step<KPL, W, G>, 32 * W * G, smem);
+            e = cudaFuncSetAttribute(lob_step<KPL, W, G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step<KPL, W, G, false>, 32 * W * G, smem);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(lob_export_l2<KPL, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      export_l2_smem_bytes<KPL, W>());
@@ -218,6 +221,22 @@ int lob_process_messages(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, i
     if (msgs_per_step == 0) n_steps = 0;
     return launch_step(ctx, d_msgs, n_steps, msgs_per_step, n_steps > 0 ? d_l2_out : nullptr, 0, ctx->cfg.n_books,
                        (cudaStream_t)stream);
+}
+
+int lob_process_messages_l1(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t msgs_per_step,
+                            int32_t *d_l2_out, int32_t *d_l1_out, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (n_steps < 0 || msgs_per_step < 0) return fail(LOB_EINVAL, "negative n_steps/msgs_per_step%s");
+    const long long nmsg = (long long)n_steps * msgs_per_step;
+    if (nmsg > (1ll << 30)) return fail(LOB_EINVAL, "n_steps*msgs_per_step overflows%s");
+    if (nmsg > 0 && ctx->cfg.n_books > 0 && (!d_msgs || !d_l1_out)) return fail(LOB_EINVAL, "d_msgs or d_l1_out is null%s");
+    if (reinterpret_cast<uintptr_t>(d_msgs) % 16 || reinterpret_cast<uintptr_t>(d_l2_out) % 16 ||
+        reinterpret_cast<uintptr_t>(d_l1_out) % 16)
+        return fail(LOB_EINVAL, "buffers must be 16-byte aligned%s");
+    if (msgs_per_step == 0) n_steps = 0;
+    return launch_step(ctx, d_msgs, n_steps, msgs_per_step, n_steps > 0 ? d_l2_out : nullptr, 0, ctx->cfg.n_books,
+                       (cudaStream_t)stream, n_steps > 0 ? d_l1_out : nullptr);
 }
 
 int lob_process_messages_host(lob_ctx *ctx, const int32_t *h_msgs, int32_t n_steps, int32_t msgs_per_step,

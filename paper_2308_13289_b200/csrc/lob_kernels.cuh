@@ -54,6 +54,7 @@ struct Params {
     long long *stats;      // [K][NST]
     const int32_t *msgs;   // [nb][n_steps*M][8]  (relative to book0)
     int32_t *l2out;        // [nb][n_steps][L][4] or null (relative to book0)
+    int32_t *l1out;        // [nb][n_steps*M][4] or null: Level-1 after every message (NEXT N1)
     unsigned *sched;       // [2]: next book, finished groups (zero between launches)
     int N, NP, Tcap, L, n_steps, M;
     int book0, nb;         // books [book0, book0+nb) of the state
@@ -210,7 +211,7 @@ struct RegBook {
 };
 
 // ------------------------------------------------------------------ the engine
-template <class BK>
+template <class BK, bool TL1 = false>
 struct Engine {
     static constexpr int KPL = BK::KPL, W = BK::W, GT = BK::GT;
     BK bk;
@@ -221,6 +222,7 @@ struct Engine {
     int xph;                // exchange buffer phase (uniform)
     // uniform best-order cache per side (Eq.5 + G1/G4): slot or BEST_*, and its price
     int bslot[2], bP[2];
+    unsigned bV[2];         // TL1: total quantity at the cached best price (its L1 volume)
     long long part_cxl;     // cancelled quantity, accumulated on the owner thread (G14)
     long long part_trd;     // traded quantity, accumulated on the owner thread
 
@@ -304,6 +306,7 @@ struct Engine {
         const int m = gmin_i(has ? lk : INT_MAX);
         // candidates at the best price: thread-local earliest (Ts, Tns, row)
         int lts = INT_MAX, ltns = INT_MAX, lj = -1, lc = 0;
+        unsigned lv = 0;
 #pragma unroll
         for (int j = 0; j < KPL; ++j) {
             const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
@@ -312,8 +315,10 @@ struct Engine {
                 const int2 t2 = bk.times(SD, j * GT + tid);
                 if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
                 ++lc;
+                lv += (unsigned)q;
             }
         }
+        if constexpr (TL1) bV[SD] = gadd(lv);
         const unsigned loc = lj < 0 ? 0xffffffffu : (unsigned)(lj * GT + tid);
         int slot;
         if (gadd((unsigned)lc) == 1) {
@@ -334,10 +339,14 @@ struct Engine {
 
     // A new order at `slot` on side SD: keep the cache exact (G4 key order).
     template <int SD>
-    __device__ __forceinline__ void note_add(int slot, int p, int ts, int tns) {
+    __device__ __forceinline__ void note_add(int slot, int p, int ts, int tns, int q) {
         const int bs = bslot[SD];
         if (bs == BEST_INVALID) return;
         bool better = bs == BEST_EMPTY;
+        if constexpr (TL1) {  // level volume: a new level, or one more order at the best price
+            if (better || ((SD == ASK) ? p < bP[SD] : p > bP[SD])) bV[SD] = (unsigned)q;
+            else if (p == bP[SD]) bV[SD] += (unsigned)q;
+        }
         if (!better) {
             const int kn = (SD == ASK) ? p : ~p, kb = (SD == ASK) ? bP[SD] : ~bP[SD];
             better = kn < kb;
@@ -368,8 +377,13 @@ struct Engine {
         const bool own = tid == (slot & (GT - 1));
         const int j = slot / GT;
         const int qi = bk.get(SD, F_Q, j);
-        if (own) part_cxl += (mQ < qi) ? mQ : qi;  // G14
+        const int cq = (mQ < qi) ? mQ : qi;
+        if (own) part_cxl += cq;                   // G14
         bk.put_if(own, SD, F_Q, j, qi - mQ);       // Q <= 0 -> empty
+        if constexpr (TL1) {                       // the level volume loses what was cancelled there
+            const int d = bcast(bk.get(SD, F_P, j) == bP[SD] ? cq : 0, slot & (GT - 1));
+            if (bslot[SD] >= 0) bV[SD] -= (unsigned)d;
+        }
         if (bslot[SD] == slot) bslot[SD] = BEST_INVALID;
     }
 
@@ -405,6 +419,7 @@ struct Engine {
             }
             ++ntr;                                                   // fills this call (logged = min(ntr, Tcap))
             bk.put_if(own, OPP, F_Q, sj, Qs2);                       // filled order removed (G10)
+            if constexpr (TL1) bV[OPP] -= (unsigned)q;
             if (Qs2 == 0) bslot[OPP] = BEST_INVALID;
         }
         if (Qa <= 0) return;
@@ -428,7 +443,19 @@ struct Engine {
         });
         // every thread stores the same record, so each later reads its own write
         bk.put_cold(OWN, slot, mTID, mTS, mTNS);
-        note_add<OWN>(slot, mP, mTS, mTNS);
+        note_add<OWN>(slot, mP, mTS, mTNS, Qa);
+    }
+
+    // NEXT N1: Level-1 after the message: the cached best of each side
+    // (recomputed if stale) and its level volume; absent side (-1, 0)
+    __device__ __forceinline__ void l1_write(int32_t *dst) {
+        if (bslot[ASK] == BEST_INVALID) recompute_best<ASK>();
+        if (bslot[BID] == BEST_INVALID) recompute_best<BID>();
+        if (tid == 0) {
+            const bool a = bslot[ASK] >= 0, b = bslot[BID] >= 0;
+            *reinterpret_cast<int4 *>(dst) = make_int4(a ? bP[ASK] : -1, a ? (int)bV[ASK] : 0, b ? bP[BID] : -1,
+                                                       b ? (int)bV[BID] : 0);
+        }
     }
 
     __device__ __forceinline__ void message(const int4 a, const int4 b) {
@@ -502,11 +529,12 @@ constexpr int step_smem_bytes() {
     return G * (2 * CH * 32 + 16 + 2 * KPL * 32 * W * 16 + ((scratch_bytes<W>() + 15) / 16) * 16);
 }
 
-// Persistent: group g of CTA b walks books (b*G + g), + gridDim.x*G, ...
-template <int KPL, int W, int G>
 #ifndef MINB4
 #define MINB4 7
 #endif
+// Persistent: group g of CTA b starts with book b*G + g, then takes books from the
+// dynamic counter.  TL1 also writes the Level-1 trace (NEXT N1).
+template <int KPL, int W, int G, bool TL1>
 __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : 16 / W))))
     lob_step(const Params p) {
     using BK = RegBook<KPL, W>;
@@ -551,7 +579,7 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
             }
         }
         if (tid < NST) sts64(scratch + 8u * tid, 0);
-        Engine<BK> e(p);
+        Engine<BK, TL1> e(p);
         e.bk.cold = cold;
         e.bk.tid = tid;
         e.tid = tid; e.book = b; e.ntr = 0; e.sc = scratch; e.xph = 0;
@@ -559,6 +587,8 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
         e.bk.load(p.book + (size_t)b * 2 * NF * BK::NP);
         e.bslot[0] = e.bslot[1] = BEST_INVALID;
         e.bP[0] = e.bP[1] = 0;
+        e.bV[0] = e.bV[1] = 0;
+        int32_t *l1dst = TL1 ? p.l1out + (size_t)lb * nmsg * 4 : nullptr;
         int left = p.M, step = 0;
         for (int c = 0; c < nchunks; ++c) {
             const uint32_t seq = chunk_seq + c, slot = seq & 1;
@@ -571,6 +601,10 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
                 do {
                     const int4 a = lds128(maddr), bb = lds128(maddr + 16);
                     e.message(a, bb);
+                    if constexpr (TL1) {
+                        e.l1_write(l1dst);
+                        l1dst += 4;
+                    }
                     maddr += 32;
                 } while (maddr != mend);
                 cnt -= run;

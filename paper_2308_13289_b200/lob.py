@@ -55,6 +55,8 @@ def lib():
             L.lob_init.argtypes = [P, P, i32, i32, i32, P]
             L.lob_process_messages.restype = ctypes.c_int
             L.lob_process_messages.argtypes = [P, P, i32, i32, P, P]
+            L.lob_process_messages_l1.restype = ctypes.c_int
+            L.lob_process_messages_l1.argtypes = [P, P, i32, i32, P, P, P]
             L.lob_process_messages_host.restype = ctypes.c_int
             L.lob_process_messages_host.argtypes = [P, P, i32, i32, P, P, P, P, i32, P]
             for name in ("lob_get_l2", "lob_get_book", "lob_get_stats"):
@@ -148,18 +150,31 @@ class LobBatch:
         self._keep = t  # keep the input alive until the stream has consumed it
 
     def process(self, msgs, n_steps: int, msgs_per_step: int, l2: bool = True, l2_out=None,
-                stream=None):
-        """lob_process_messages over msgs [K][n_steps*msgs_per_step][8]; returns L2 [K][S][L][4]."""
+                stream=None, l1: bool = False, l1_out=None):
+        """lob_process_messages over msgs [K][n_steps*msgs_per_step][8]; returns L2 [K][S][L][4].
+
+        With ``l1=True`` (lob_process_messages_l1, NEXT row N1) returns ``(l2, l1)`` where
+        l1 [K][n_steps*msgs_per_step][4] is the Level-1 state after every message."""
         m = self._dev(msgs)
         assert m.shape == (self.K, n_steps * msgs_per_step, 8), m.shape
         out = l2_out
         if l2 and out is None:
             out = torch.empty((self.K, n_steps, self.L, 4), dtype=torch.int32, device=self.device)
+        l1o = l1_out
+        if l1 and l1o is None:
+            l1o = torch.empty((self.K, n_steps * msgs_per_step, 4), dtype=torch.int32, device=self.device)
         with torch.cuda.device(self.device):
-            _check(lib().lob_process_messages(self.ctx, _ptr(m), int(n_steps), int(msgs_per_step),
-                                              _ptr(out) if l2 else None, _stream(stream)),
-                   "lob_process_messages")
+            if l1:
+                _check(lib().lob_process_messages_l1(self.ctx, _ptr(m), int(n_steps), int(msgs_per_step),
+                                                     _ptr(out) if l2 else None, _ptr(l1o), _stream(stream)),
+                       "lob_process_messages_l1")
+            else:
+                _check(lib().lob_process_messages(self.ctx, _ptr(m), int(n_steps), int(msgs_per_step),
+                                                  _ptr(out) if l2 else None, _stream(stream)),
+                       "lob_process_messages")
         self._keep = m
+        if l1:
+            return (out if l2 else None), l1o
         return out if l2 else None
 
     def process_host(self, h_msgs, n_steps: int, msgs_per_step: int, h_l2_out=None,

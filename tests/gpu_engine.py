@@ -16,10 +16,13 @@ class GpuEngine:
         self.b.init(None if init_l2 is None else torch.from_numpy(np.ascontiguousarray(init_l2)),
                     init_ts, init_tns)
 
-    def process(self, msgs, n_steps, msgs_per_step, l2=True):
+    def process(self, msgs, n_steps, msgs_per_step, l2=True, l1=False):
         out = self.b.process(torch.from_numpy(np.ascontiguousarray(msgs, dtype=np.int32)),
-                             n_steps, msgs_per_step, l2=l2)
+                             n_steps, msgs_per_step, l2=l2, l1=l1)
         torch.cuda.synchronize()
+        if l1:
+            a, b = out
+            return (None if a is None else a.cpu().numpy()), b.cpu().numpy()
         return None if out is None else out.cpu().numpy()
 
     def book(self):

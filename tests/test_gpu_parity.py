@@ -147,3 +147,26 @@ def test_full_size_c4_sampled_books():
     l2 = g["l2"]
     both = (l2[..., 0] > 0) & (l2[..., 2] > 0)
     assert (l2[..., 0, 0][both[..., 0]] > l2[..., 0, 2][both[..., 0]]).all()  # never crossed
+
+
+# ------------------------------------------- NEXT row N1: per-message Level-1 trace
+@pytest.mark.parametrize("name,n,profile", [("C4", 700, None), ("C3", 400, None), ("C5_32", 300, None),
+                                            ("C5_512", 80, None), ("C5_2048", 12, None),
+                                            ("C1", 1, "ties"), ("C1", 1, "garbage"), ("C1", 1, "synthetic"),
+                                            ("C5_100", 200, "overflow")])
+def test_l1_trace(name, n, profile):
+    cfg = lobgen.CONFIGS[name].with_(n_books=n)
+    if profile:
+        cfg = cfg.with_(profile=profile, n_books=150, capacity=60, init_levels=12)
+    msgs, init = lobgen.generate(cfg)
+    g = GpuEngine(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
+    o = oracle.OracleBatch(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels, threads=8)
+    res = []
+    for e in (g, o):
+        e.init(init, lobgen.INIT_TS, lobgen.INIT_TNS)
+        l2, l1 = e.process(msgs, cfg.n_steps, cfg.msgs_per_step, l1=True)
+        res.append((l2, l1, e.book(), e.stats()))
+    for a, b, what in zip(res[0], res[1], ("l2", "l1", "book", "stats")):
+        if not np.array_equal(a, b):
+            bad = np.argwhere(a != b)
+            raise AssertionError(f"{name}/{profile}: {what} differs at {len(bad)} positions, first {bad[:4].tolist()}")
