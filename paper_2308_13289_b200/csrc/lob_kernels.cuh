@@ -333,8 +333,12 @@ struct Engine {
         bslot[SD] = slot;
         bP[SD] = (SD == ASK) ? m : ~m;
         const int2 bt = bk.times(SD, slot);  // broadcast shared load
-        sts32(bt_addr(SD, 0), bt.x);         // every thread stores the same value
-        sts32(bt_addr(SD, 1), bt.y);
+        group_sync<W>();                     // earlier readers of bt are done
+        if (tid == 0) {                      // one writer, published to the group
+            sts32(bt_addr(SD, 0), bt.x);
+            sts32(bt_addr(SD, 1), bt.y);
+        }
+        group_sync<W>();
     }
 
     // A new order at `slot` on side SD: keep the cache exact (G4 key order).
@@ -357,8 +361,12 @@ struct Engine {
         }
         if (better) {
             bslot[SD] = slot; bP[SD] = p;
-            sts32(bt_addr(SD, 0), ts);
-            sts32(bt_addr(SD, 1), tns);
+            group_sync<W>();
+            if (tid == 0) {
+                sts32(bt_addr(SD, 0), ts);
+                sts32(bt_addr(SD, 1), tns);
+            }
+            group_sync<W>();
         }
     }
 
@@ -441,8 +449,8 @@ struct Engine {
                 bk.v[OWN][F_OID][J] = mOID;
             }
         });
-        // every thread stores the same record, so each later reads its own write
-        bk.put_cold(OWN, slot, mTID, mTS, mTNS);
+        if (tid == 0) bk.put_cold(OWN, slot, mTID, mTS, mTNS);  // one writer, published below
+        group_sync<W>();
         note_add<OWN>(slot, mP, mTS, mTNS, Qa);
     }
 

@@ -1,0 +1,43 @@
+#!/usr/bin/env python
+"""Small parity run for compute-sanitizer (memcheck/racecheck/synccheck/initcheck):
+every book geometry (W = 1 and W > 1), L2 + L1 outputs, exports, the host path."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import lobgen  # noqa: E402
+import oracle  # noqa: E402
+from gpu_engine import GpuEngine  # noqa: E402
+
+fails = 0
+for N, K, prof in [(100, 9, "lobster"), (33, 5, "garbage"), (200, 3, "heavy_market"), (512, 2, "ties"),
+                   (2048, 1, "lobster")]:
+    cfg = lobgen.Config("san", K, N, 2, 20, min(N, 10), 16, 4, prof, 3)
+    msgs, init = lobgen.generate(cfg)
+    g, o = GpuEngine(K, N, 16, 4), oracle.OracleBatch(K, N, 16, 4)
+    out = []
+    for e in (g, o):
+        e.init(init, lobgen.INIT_TS, lobgen.INIT_TNS)
+        l2, l1 = e.process(msgs, cfg.n_steps, cfg.msgs_per_step, l1=True)
+        l2b = e.process(msgs, cfg.n_steps, cfg.msgs_per_step)
+        out.append((l2, l1, l2b, e.book(), e.trades()[0], e.l2(), e.stats()))
+    ok = all(np.array_equal(a, b) for a, b in zip(*out))
+    fails += not ok
+    print(N, K, prof, "ok" if ok else "MISMATCH", flush=True)
+from paper_2308_13289_b200 import LobBatch  # noqa: E402
+cfg = lobgen.CONFIGS["C4"].with_(n_books=40)
+msgs, init = lobgen.generate(cfg)
+b = LobBatch(40, 100, cfg.trades_cap, 10)
+b.init(torch.from_numpy(init).cuda(), lobgen.INIT_TS, lobgen.INIT_TNS)
+h = torch.from_numpy(msgs).pin_memory()
+hl2 = torch.empty((40, cfg.n_steps, 10, 4), dtype=torch.int32).pin_memory()
+b.process_host(h, cfg.n_steps, cfg.msgs_per_step, hl2, None, torch.empty_like(h, device="cuda"),
+               torch.empty_like(hl2, device="cuda"), chunks=3)
+torch.cuda.synchronize()
+print("host path ok")
+sys.exit(1 if fails else 0)
