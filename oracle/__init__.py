@@ -61,6 +61,7 @@ def _load():
                          "oracle_get_violations"):
                 getattr(lib, name).argtypes = [P, P]
             lib.oracle_get_trades.argtypes = [P, P, P]
+            lib.oracle_step_reward.argtypes = [P, P, P, P, ctypes.c_double, P, P, P]
             _lib = lib
     return _lib
 
@@ -142,6 +143,15 @@ class OracleBatch:
         out = np.empty((self.K, NSTATS), np.int64)
         self.lib.oracle_get_stats(self.ctx, _ptr(out))
         return out
+
+    def step_reward(self, agent_oids, p_init, side, lam: float):
+        """NEXT row N2 over the last call's trade log: (reward f64[K], vwap f64[K], agent_qty i64[K])."""
+        a = np.ascontiguousarray(agent_oids, dtype=np.int32).reshape(self.K, 2)
+        pi = np.ascontiguousarray(p_init, dtype=np.float64).reshape(self.K)
+        sd = np.ascontiguousarray(side, dtype=np.int32).reshape(self.K)
+        r, v, q = np.empty(self.K), np.empty(self.K), np.empty(self.K, np.int64)
+        self.lib.oracle_step_reward(self.ctx, _ptr(a), _ptr(pi), _ptr(sd), float(lam), _ptr(r), _ptr(v), _ptr(q))
+        return r, v, q
 
     def violations(self) -> np.ndarray:
         out = np.empty((self.K,), np.int64)

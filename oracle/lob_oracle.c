@@ -426,6 +426,44 @@ int oracle_process(oracle_ctx *X, int32_t k0, int32_t k1, const int32_t *msgs, i
     return oracle_process_ex(X, k0, k1, msgs, n_steps, M, l2_out, NULL);
 }
 
+/* NEXT row N2: step reward over the trade log of the last call (one env step).
+ *   P_VWAP = sum_i Q_i P_i / sum_i Q_i over every logged trade i     (eq:vwap)
+ *   R      = sum_j Q_j (P_j - P_VWAP) + lambda sum_j Q_j (P_VWAP - P_init)
+ *                                                                  (eq:rewardfunc)
+ * j = the agent's trades: aggressor or standing OID in [agent_lo, agent_hi] (reading G29);
+ * side -1 = sell task (the paper's form), +1 = buy task: both terms negated (G30);
+ * no trades in the step: P_VWAP = 0 and R = 0 (G31).  Double precision, trade-log order. */
+void oracle_step_reward(oracle_ctx *X, const int32_t *agent /*[K][2]*/, const double *p_init /*[K]*/,
+                        const int32_t *side /*[K]*/, double lambda, double *reward, double *vwap,
+                        int64_t *agent_qty) {
+    for (int k = 0; k < X->K; k++) {
+        const obook *b = &X->books[k];
+        double sqp = 0.0, sq = 0.0;
+        for (int i = 0; i < b->n_trades; i++) {
+            const int32_t *t = b->trades + (size_t)i * T_NF;
+            sqp += (double)t[1] * (double)t[0];
+            sq += (double)t[1];
+        }
+        double v = (sq > 0.0) ? sqp / sq : 0.0;
+        double adv = 0.0, drift = 0.0;
+        int64_t qa = 0;
+        int32_t lo = agent[2 * k], hi = agent[2 * k + 1];
+        for (int i = 0; i < b->n_trades && sq > 0.0; i++) {
+            const int32_t *t = b->trades + (size_t)i * T_NF;
+            int mine = (t[2] >= lo && t[2] <= hi) || (t[3] >= lo && t[3] <= hi);
+            if (!mine) continue;
+            adv += (double)t[1] * ((double)t[0] - v);
+            drift += (double)t[1] * (v - p_init[k]);
+            qa += t[1];
+        }
+        double r = adv + lambda * drift;
+        if (side[k] == 1) r = -r;
+        if (reward) reward[k] = r;
+        if (vwap) vwap[k] = v;
+        if (agent_qty) agent_qty[k] = qa;
+    }
+}
+
 /* exports: book [K][2][N][6] (side 0 = asks), trades [K][T_cap][6] + counts,
  * current L2 [K][L][4], counters [K][10], invariant violations [K] */
 void oracle_get_book(oracle_ctx *X, int32_t *out) {
