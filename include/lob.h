@@ -125,6 +125,24 @@ int lob_process_messages_host(lob_ctx *ctx, const int32_t *h_msgs, int32_t n_ste
                               int32_t *d_msgs_buf, int32_t *d_l2_buf, int32_t chunks,
                               void *cuda_stream);
 
+/* NEXT row N2: step reward epilogue over the trade log of the
+ * last lob_process_messages call (= one env step when called once per step,
+ * G9).  Per book k, over the logged trades i and the agent's trades j:
+ *   P_VWAP = sum_i Q_i P_i / sum_i Q_i                         (eq:vwap)
+ *   R      = sum_j Q_j (P_j - P_VWAP) + lambda sum_j Q_j (P_VWAP - P_init)
+ *                                                             (eq:rewardfunc)
+ *  d_agent_oids: [K][2] int32 inclusive OID range of the agent's orders; a trade is
+ *                the agent's if its aggressor or standing OID lies in it (G29).
+ *  d_p_init:     [K] f64 initial mid price of the episode.
+ *  d_task_side:  [K] int32, -1 sell task (the paper's form), +1 buy task (R negated, G30).
+ *  Outputs (each nullable): d_reward [K] f64, d_vwap [K] f64, d_agent_qty [K] int64
+ *  (executed agent quantity).  A step without trades gives R = 0, P_VWAP = 0 (G31).
+ *  Double precision; P_VWAP is exact up to one rounding, R agrees with the serial
+ *  definition to 1e-12 of the magnitude of its terms. */
+int lob_step_reward(lob_ctx *ctx, const int32_t *d_agent_oids, const double *d_p_init,
+                    const int32_t *d_task_side, double lambda, double *d_reward, double *d_vwap,
+                    int64_t *d_agent_qty, void *cuda_stream);
+
 /* Current L2 snapshot of every book: d_out [K][L][4] int32. */
 int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *cuda_stream);
 

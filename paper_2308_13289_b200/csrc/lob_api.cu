@@ -309,6 +309,23 @@ int lob_process_messages_host(lob_ctx *ctx, const int32_t *h_msgs, int32_t n_ste
     return rc;
 }
 
+int lob_step_reward(lob_ctx *ctx, const int32_t *d_agent_oids, const double *d_p_init, const int32_t *d_task_side,
+                    double lambda, double *d_reward, double *d_vwap, int64_t *d_agent_qty, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    if (!d_agent_oids || !d_p_init || !d_task_side) return fail(LOB_EINVAL, "agent range, p_init and side are required%s");
+    if (reinterpret_cast<uintptr_t>(d_p_init) % 8 || reinterpret_cast<uintptr_t>(d_reward) % 8 ||
+        reinterpret_cast<uintptr_t>(d_vwap) % 8 || reinterpret_cast<uintptr_t>(d_agent_qty) % 8)
+        return fail(LOB_EINVAL, "double / int64 buffers must be 8-byte aligned%s");
+    const int wpb = 8;
+    lob_reward_kernel<<<blocks_for(K, wpb), wpb * 32, 0, (cudaStream_t)stream>>>(
+        ctx->trades(), ctx->ntr(), K, ctx->cfg.trades_cap, d_agent_oids, d_p_init, d_task_side, lambda, d_reward,
+        d_vwap, reinterpret_cast<long long *>(d_agent_qty));
+    return after_launch("lob_reward_kernel");
+}
+
 int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *stream) {
     int rc = check_ctx(ctx);
     if (rc) return rc;

@@ -716,6 +716,58 @@ __global__ void lob_init_kernel(int32_t *book, int32_t *trades, int32_t *ntrades
     }
 }
 
+// NEXT row N2: step reward over the last call's trade log (one env step), one warp
+// per book.  P_VWAP = sum_i Q_i P_i / sum_i Q_i (eq:vwap): both sums are
+// exact in double (integer products < 2^53), so P_VWAP is correctly rounded whatever
+// the summation order.  R = sum_j Q_j (P_j - P_VWAP) + lambda sum_j Q_j (P_VWAP -
+// P_init) over the agent's trades j (eq:rewardfunc; agent = aggressor or
+// standing OID in the book's range, G29); buy task negates (G30); no trades -> 0 (G31).
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    return x;
+}
+__global__ void lob_reward_kernel(const int32_t *trades, const int32_t *ntrades, int K, int Tcap,
+                                  const int32_t *agent, const double *p_init, const int32_t *side, double lambda,
+                                  double *reward, double *vwap, long long *agent_qty) {
+    const int lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= K) return;
+    const int n = ntrades[b];
+    const int2 *t = reinterpret_cast<const int2 *>(trades + (size_t)b * Tcap * 6);
+    double sqp = 0.0, sq = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const int2 pq = t[3 * i];
+        sqp += (double)pq.y * (double)pq.x;
+        sq += (double)pq.y;
+    }
+    sqp = warp_sum(sqp);
+    sq = warp_sum(sq);
+    const double v = sq > 0.0 ? sqp / sq : 0.0;
+    const int lo = agent[2 * b], hi = agent[2 * b + 1];
+    const double p0 = p_init[b];
+    double adv = 0.0, drift = 0.0;
+    long long qa = 0;
+    for (int i = lane; i < n && sq > 0.0; i += 32) {
+        const int2 pq = t[3 * i], oo = t[3 * i + 1];
+        if ((oo.x >= lo && oo.x <= hi) || (oo.y >= lo && oo.y <= hi)) {
+            adv += (double)pq.y * ((double)pq.x - v);
+            drift += (double)pq.y * (v - p0);
+            qa += pq.y;
+        }
+    }
+    adv = warp_sum(adv);
+    drift = warp_sum(drift);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qa += __shfl_xor_sync(FULL, qa, o);
+    if (lane == 0) {
+        const double r = adv + lambda * drift;
+        if (reward) reward[b] = side[b] == 1 ? -r : r;
+        if (vwap) vwap[b] = v;
+        if (agent_qty) agent_qty[b] = qa;
+    }
+}
+
 // book export: SoA (internal) -> [K][2][N][6] AoS; one thread per (book, side, slot)
 __global__ void lob_export_book(const int32_t *book, int32_t *out, int K, int N, int NP) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;

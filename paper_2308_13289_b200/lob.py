@@ -64,6 +64,8 @@ def lib():
                 getattr(L, name).argtypes = [P, P, P]
             L.lob_get_trades.restype = ctypes.c_int
             L.lob_get_trades.argtypes = [P, P, P, P]
+            L.lob_step_reward.restype = ctypes.c_int
+            L.lob_step_reward.argtypes = [P, P, P, P, ctypes.c_double, P, P, P, P]
             L.lob_launch_count.restype = ctypes.c_int64
             L.lob_strerror.restype = ctypes.c_char_p
             L.lob_strerror.argtypes = [ctypes.c_int]
@@ -186,6 +188,23 @@ class LobBatch:
                 self.ctx, _ptr(h_msgs), int(n_steps), int(msgs_per_step), _ptr(h_l2_out),
                 _ptr(h_stats_out), _ptr(d_msgs_buf), _ptr(d_l2_buf), int(chunks), _stream(stream)),
                 "lob_process_messages_host")
+
+    def step_reward(self, agent_oids, p_init, task_side, lam: float, stream=None):
+        """lob_step_reward (NEXT row N2) over the last call's trade log.
+
+        agent_oids [K][2] int32 (inclusive OID range), p_init [K] f64, task_side [K]
+        int32 (-1 sell, +1 buy).  Returns (reward f64[K], vwap f64[K], agent_qty i64[K])."""
+        a = self._dev(agent_oids)
+        pi = self._dev(p_init, torch.float64)
+        sd = self._dev(task_side)
+        r = torch.empty((self.K,), dtype=torch.float64, device=self.device)
+        v = torch.empty_like(r)
+        q = torch.empty((self.K,), dtype=torch.int64, device=self.device)
+        with torch.cuda.device(self.device):
+            _check(lib().lob_step_reward(self.ctx, _ptr(a), _ptr(pi), _ptr(sd), float(lam), _ptr(r), _ptr(v),
+                                         _ptr(q), _stream(stream)), "lob_step_reward")
+        self._keep = (a, pi, sd)
+        return r, v, q
 
     def l2(self, stream=None):
         out = torch.empty((self.K, self.L, 4), dtype=torch.int32, device=self.device)

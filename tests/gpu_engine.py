@@ -35,6 +35,12 @@ class GpuEngine:
     def l2(self):
         return self.b.l2().cpu().numpy()
 
+    def step_reward(self, agent_oids, p_init, side, lam):
+        r, v, q = self.b.step_reward(torch.as_tensor(np.asarray(agent_oids, np.int32)),
+                                     torch.as_tensor(np.asarray(p_init, np.float64)),
+                                     torch.as_tensor(np.asarray(side, np.int32)), lam)
+        return r.cpu().numpy(), v.cpu().numpy(), q.cpu().numpy()
+
     def stats(self):
         return self.b.stats().cpu().numpy()
 

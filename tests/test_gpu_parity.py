@@ -170,3 +170,43 @@ def test_l1_trace(name, n, profile):
         if not np.array_equal(a, b):
             bad = np.argwhere(a != b)
             raise AssertionError(f"{name}/{profile}: {what} differs at {len(bad)} positions, first {bad[:4].tolist()}")
+
+
+# ------------------------------------------------- NEXT row N2: step reward epilogue
+def test_reward_golden_on_gpu():
+    from test_reward_pins import DOC, _run_fixture
+    eng = _run_fixture(lambda K, N, T, L: GpuEngine(K, N, T, L))
+    for c in DOC["cases"]:
+        r, v, q = eng.step_reward([c["agent"]], [c["p_init"]], [c["side"]], c["lambda"])
+        assert r[0] == c["reward"] and v[0] == c["vwap"] and q[0] == c["agent_qty"], c
+
+
+@pytest.mark.parametrize("name,n", [("C3", 3000), ("C2", 1000), ("C5_512", 60)])
+def test_reward_parity(name, n):
+    """P_VWAP and the agent quantity are exact (bit-equal); R within 1e-12 of the
+    magnitude of its terms (summation order differs: lane-strided + warp tree)."""
+    cfg = lobgen.CONFIGS[name].with_(n_books=n, n_steps=1)
+    msgs, init = lobgen.generate(cfg)
+    rng = np.random.default_rng(7)
+    lo = rng.integers(1, 60, n).astype(np.int32)
+    agent = np.stack([lo, lo + rng.integers(0, 40, n).astype(np.int32)], 1)
+    p_init = rng.uniform(9.9e5, 1.01e6, n)
+    side = rng.choice([-1, 1], n).astype(np.int32)
+    g = GpuEngine(n, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
+    o = oracle.OracleBatch(n, cfg.capacity, cfg.trades_cap, cfg.l2_levels, threads=8)
+    for e in (g, o):
+        e.init(init, lobgen.INIT_TS, lobgen.INIT_TNS)
+        e.process(msgs, cfg.n_steps, cfg.msgs_per_step)
+    tr, cnt = o.trades()
+    for lam in (0.0, 1.0, 0.25):
+        rg, vg, qg = g.step_reward(agent, p_init, side, lam)
+        ro, vo, qo = o.step_reward(agent, p_init, side, lam)
+        np.testing.assert_array_equal(vg, vo)
+        np.testing.assert_array_equal(qg, qo)
+        for k in range(n):
+            t = tr[k, :cnt[k]]
+            mine = ((t[:, 2] >= agent[k, 0]) & (t[:, 2] <= agent[k, 1])) | \
+                   ((t[:, 3] >= agent[k, 0]) & (t[:, 3] <= agent[k, 1]))
+            q = t[mine, 1].astype(np.float64)
+            scale = (q * (np.abs(t[mine, 0]) + abs(vo[k]))).sum() + abs(lam) * (q * (abs(vo[k]) + p_init[k])).sum()
+            assert abs(rg[k] - ro[k]) <= 1e-12 * max(scale, 1.0), (k, lam, rg[k], ro[k])
