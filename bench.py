@@ -281,12 +281,23 @@ def main():
                 "alg_bytes_per_launch": alg_bytes, "alg_bytes_per_msg": alg_bytes / (K * cfg.n_msgs),
                 "peak_source": peak_src}
     prof = os.path.join(ROOT, "profiles", "traffic.json")
+    roofline_issue = None
     if os.path.exists(prof):
         try:
             tr = json.load(open(prof)).get(cfg.name)
             if tr:
                 roofline["traffic"] = tr["dram_bytes_per_launch"]
                 roofline["traffic_source"] = tr["source"]
+                # the bound that actually binds: warp-instruction issue
+                ipm = tr.get("warp_instructions_per_msg")
+                if ipm:
+                    _, _, max_mhz = load_peaks()
+                    peak_issue = 148 * 4 * max_mhz * 1e6 / 1e12            # warp-instr/ps -> T/s
+                    ach = ipm * K * cfg.n_msgs / (kmean_ms / 1e3) / 1e12
+                    roofline_issue = {"bound": "alu", "achieved": ach, "peak": peak_issue,
+                                      "unit": "Twarp-instr/s", "frac": ach / peak_issue,
+                                      "warp_instructions_per_msg": ipm, "source": tr.get("instr_source"),
+                                      "peak_derivation": "148 SMs x 4 schedulers x 1 warp-instr/clk x sm_max_mhz"}
         except Exception:
             pass
 
@@ -335,7 +346,8 @@ def main():
                            "profile": cfg.profile, "seed": cfg.seed, "parallelism": f"books sharded x{world}",
                            "l2_flush": "inputs larger than L2 (messages %.2f GB/GPU > 126 MB)"
                                        % (msgs_h.numel() * 4 / 1e9)},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": n_launch,
+                "roofline": roofline, "roofline_issue": roofline_issue, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": n_launch,
                 "clocks": sampler.summary(),
                 "totals": dict(zip(["msgs", "bad", "trades", "trades_dropped", "traded_qty", "cancelled_qty",
                                     "unknown_cancels", "add_overflow", "overflow_qty", "market_discarded_qty"],
