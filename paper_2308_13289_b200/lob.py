@@ -55,8 +55,9 @@ def lib():
             L.lob_init.argtypes = [P, P, i32, i32, i32, P]
             L.lob_process_messages.restype = ctypes.c_int
             L.lob_process_messages.argtypes = [P, P, i32, i32, P, P]
-            L.lob_process_messages_l1.restype = ctypes.c_int
-            L.lob_process_messages_l1.argtypes = [P, P, i32, i32, P, P, P]
+            if hasattr(L, "lob_process_messages_l1"):  # (absent only in old A/B builds)
+                L.lob_process_messages_l1.restype = ctypes.c_int
+                L.lob_process_messages_l1.argtypes = [P, P, i32, i32, P, P, P]
             L.lob_process_messages_host.restype = ctypes.c_int
             L.lob_process_messages_host.argtypes = [P, P, i32, i32, P, P, P, P, i32, P]
             for name in ("lob_get_l2", "lob_get_book", "lob_get_stats"):
@@ -64,8 +65,9 @@ def lib():
                 getattr(L, name).argtypes = [P, P, P]
             L.lob_get_trades.restype = ctypes.c_int
             L.lob_get_trades.argtypes = [P, P, P, P]
-            L.lob_step_reward.restype = ctypes.c_int
-            L.lob_step_reward.argtypes = [P, P, P, P, ctypes.c_double, P, P, P, P]
+            if hasattr(L, "lob_step_reward"):
+                L.lob_step_reward.restype = ctypes.c_int
+                L.lob_step_reward.argtypes = [P, P, P, P, ctypes.c_double, P, P, P, P]
             L.lob_launch_count.restype = ctypes.c_int64
             L.lob_strerror.restype = ctypes.c_char_p
             L.lob_strerror.argtypes = [ctypes.c_int]
