@@ -17,6 +17,9 @@ import tempfile
 
 rep, fn = sys.argv[1], sys.argv[2]
 dump = len(sys.argv) > 3 and sys.argv[3] == "dump"
+alu_only = os.environ.get("ALU_ONLY") == "1"
+ALU_OPS = ("ISETP", "SEL", "LOP3", "IADD3", "SHF", "PRMT", "IMNMX", "VIMNMX", "FLO", "POPC", "PLOP3", "P2R", "R2P",
+           "VIADD", "LEA", "ICMP", "BMSK", "SGXT", "MOV ")
 top = int(sys.argv[3]) if len(sys.argv) > 3 and not dump else 40
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 so = os.path.join(root, "paper_2308_13289_b200", "liblob.so")
@@ -78,6 +81,9 @@ src = open(os.path.join(root, "paper_2308_13289_b200", "csrc", "lob_kernels.cuh"
 agg_i, agg_s = collections.Counter(), collections.Counter()
 total = sum(counts.values())
 for a, c in counts.items():
+    if alu_only and not any(line_of.get(a, (None, None, ""))[2].lstrip("@!P0123456789T ").startswith(op)
+                            for op in ALU_OPS):
+        continue
     inner = line_of.get(a, (None, None, ""))[0]
     agg_i[inner] += c
     agg_s[inner] += stalls.get(a, 0)
