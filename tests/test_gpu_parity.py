@@ -210,3 +210,39 @@ def test_reward_parity(name, n):
             q = t[mine, 1].astype(np.float64)
             scale = (q * (np.abs(t[mine, 0]) + abs(vo[k]))).sum() + abs(lam) * (q * (abs(vo[k]) + p_init[k])).sum()
             assert abs(rg[k] - ro[k]) <= 1e-12 * max(scale, 1.0), (k, lam, rg[k], ro[k])
+
+
+# ---------------------------------------------- NEXT row N4: LOBSTER files -> engine
+def test_lobster_windows_end_to_end(tmp_path):
+    """A synthetic LOBSTER day (message + orderbook CSV) is parsed, cut into windows
+    (each window one independent book) and replayed on the GPU and the
+    oracle: bit-exact."""
+    import os
+    from paper_2308_13289_b200 import lobster
+    cfg = lobgen.CONFIGS["C4"].with_(n_books=1, n_steps=30, msgs_per_step=100)
+    msgs, init = lobgen.generate(cfg)
+    text = lobster.format_messages(msgs[0])
+    mp = os.path.join(tmp_path, "day_message_10.csv")
+    open(mp, "w").write(text)
+    m, rows, _ = lobster.parse_messages(mp)
+    rng = np.random.default_rng(4)
+    ob = np.zeros((len(m), 40), np.int64)
+    for lv in range(10):
+        ob[:, 4 * lv:4 * lv + 4] = [lobgen.REF0 + (lv + 1) * 100, 0, lobgen.REF0 - (lv + 1) * 100, 0]
+        ob[:, 4 * lv + 1] = rng.integers(1, 500, len(m))
+        ob[:, 4 * lv + 3] = rng.integers(1, 500, len(m))
+    obp = os.path.join(tmp_path, "day_orderbook_10.csv")
+    np.savetxt(obp, ob, fmt="%d", delimiter=",")
+    book = lobster.parse_orderbook(obp, 10)
+    w = lobster.build_windows(m, rows, book, window_s=3, msgs_per_step=100, start_s=int(m[0, 6]),
+                              end_s=int(m[-1, 6]) + 1)
+    K = w.msgs.shape[0]
+    assert K >= 2 and w.real_steps.sum() > 0
+    g = GpuEngine(K, 100, 512, 10)
+    o = oracle.OracleBatch(K, 100, 512, 10)
+    res = []
+    for e in (g, o):
+        e.init(w.init_l2, 34200, 0)
+        res.append((e.process(w.msgs, w.n_steps, w.msgs_per_step), e.book(), e.stats()))
+    for a, b in zip(*res):
+        np.testing.assert_array_equal(a, b)
