@@ -222,6 +222,10 @@ struct Engine {
     int xph;                // exchange buffer phase (uniform)
     // uniform best-order cache per side (Eq.5 + G1/G4): slot or BEST_*, and its price
     int bslot[2], bP[2];
+    // best order's (Ts, Tns): uniform registers for multi-warp books (no barriers),
+    // shared memory for warp books (saves 4 registers on the 72-register kernel)
+    static constexpr bool kBtRegs = (W > 1);
+    int bTS[2], bTNS[2];
     unsigned bV[2];         // TL1: total quantity at the cached best price (its L1 volume)
     long long part_cxl;     // cancelled quantity, accumulated on the owner thread (G14)
     long long part_trd;     // traded quantity, accumulated on the owner thread
@@ -333,12 +337,20 @@ struct Engine {
         bslot[SD] = slot;
         bP[SD] = (SD == ASK) ? m : ~m;
         const int2 bt = bk.times(SD, slot);  // broadcast shared load
-        group_sync<W>();                     // earlier readers of bt are done
-        if (tid == 0) {                      // one writer, published to the group
-            sts32(bt_addr(SD, 0), bt.x);
-            sts32(bt_addr(SD, 1), bt.y);
+        set_bt<SD>(bt.x, bt.y);
+    }
+    template <int SD>
+    __device__ __forceinline__ void set_bt(int ts, int tns) {
+        if constexpr (kBtRegs) {
+            bTS[SD] = ts; bTNS[SD] = tns;
+        } else {
+            group_sync<W>();                 // earlier readers of bt are done
+            if (tid == 0) {                  // one writer, published to the group
+                sts32(bt_addr(SD, 0), ts);
+                sts32(bt_addr(SD, 1), tns);
+            }
+            group_sync<W>();
         }
-        group_sync<W>();
     }
 
     // A new order at `slot` on side SD: keep the cache exact (G4 key order).
@@ -355,18 +367,14 @@ struct Engine {
             const int kn = (SD == ASK) ? p : ~p, kb = (SD == ASK) ? bP[SD] : ~bP[SD];
             better = kn < kb;
             if (kn == kb) {  // same price: time, then slot (G4)
-                const int bts = lds32(bt_addr(SD, 0)), btns = lds32(bt_addr(SD, 1));
+                const int bts = kBtRegs ? bTS[SD] : lds32(bt_addr(SD, 0));
+                const int btns = kBtRegs ? bTNS[SD] : lds32(bt_addr(SD, 1));
                 better = ts < bts || (ts == bts && (tns < btns || (tns == btns && slot < bs)));
             }
         }
         if (better) {
             bslot[SD] = slot; bP[SD] = p;
-            group_sync<W>();
-            if (tid == 0) {
-                sts32(bt_addr(SD, 0), ts);
-                sts32(bt_addr(SD, 1), tns);
-            }
-            group_sync<W>();
+            set_bt<SD>(ts, tns);
         }
     }
 
