@@ -22,7 +22,7 @@ $(PKG)/liblobster.so: $(PKG)/csrc/lobster_io.c
 	gcc -O2 -std=c11 -Wall -shared -fPIC -o $@ $<
 
 oracle/liblob_oracle.so: oracle/lob_oracle.c
-	gcc -O2 -std=c11 -Wall -shared -fPIC -o $@ $<
+	gcc -O2 -std=c11 -Wall -shared -fPIC -o $@ $< -lm
 
 lobgen/liblobgen.so: lobgen/lobgen.c
 	gcc -O2 -std=c11 -Wall -shared -fPIC -pthread -o $@ $<

@@ -35,7 +35,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC",
-                               "-o", tmp, _SRC])
+                               "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -62,6 +62,12 @@ def _load():
                 getattr(lib, name).argtypes = [P, P]
             lib.oracle_get_trades.argtypes = [P, P, P]
             lib.oracle_step_reward.argtypes = [P, P, P, P, ctypes.c_double, P, P, P]
+            lib.oracle_env_create.restype = P
+            lib.oracle_env_create.argtypes = [i32]
+            lib.oracle_env_destroy.argtypes = [P]
+            lib.oracle_env_reset.argtypes = [P, P, P, i32, i32]
+            lib.oracle_env_step.argtypes = [P, P, P, P, P, i32, P, P, P, P]
+            lib.oracle_env_get.argtypes = [P, P, P]
             _lib = lib
     return _lib
 
@@ -156,4 +162,42 @@ class OracleBatch:
     def violations(self) -> np.ndarray:
         out = np.empty((self.K,), np.int64)
         self.lib.oracle_get_violations(self.ctx, _ptr(out))
+        return out
+
+
+class EnvConfig(ctypes.Structure):
+    """NEXT row N3 execution-env parameters (common to all envs)."""
+    _fields_ = [("task_side", ctypes.c_int32), ("task_size", ctypes.c_int32), ("n_passive", ctypes.c_int32),
+                ("tick", ctypes.c_int32), ("episode_s", ctypes.c_int32), ("agent_tid", ctypes.c_int32),
+                ("oid_base", ctypes.c_int32), ("pad", ctypes.c_int32), ("lam", ctypes.c_double)]
+
+
+class OracleEnv:
+    """One execution environment per book of an OracleBatch (Sec.5.1.3, 5.2)."""
+
+    def __init__(self, batch: OracleBatch, cfg: EnvConfig):
+        self.b, self.cfg, self.lib = batch, cfg, batch.lib
+        self.env = self.lib.oracle_env_create(batch.K)
+
+    def __del__(self):
+        e, self.env = getattr(self, "env", None), None
+        if e:
+            self.lib.oracle_env_destroy(e)
+
+    def reset(self, init_ts: int, init_tns: int = 0):
+        self.lib.oracle_env_reset(self.b.ctx, self.env, ctypes.byref(self.cfg), int(init_ts), int(init_tns))
+
+    def step(self, actions, data, M: int):
+        K = self.b.K
+        a = np.ascontiguousarray(actions, dtype=np.float32).reshape(K, 4)
+        d = np.ascontiguousarray(data, dtype=np.int32).reshape(K, M, 8)
+        r, dn, ex = np.empty(K), np.empty(K, np.int32), np.empty(K, np.int64)
+        am = np.empty((K, 8, 8), np.int32)
+        self.lib.oracle_env_step(self.b.ctx, self.env, ctypes.byref(self.cfg), _ptr(a), _ptr(d), M, _ptr(r),
+                                 _ptr(dn), _ptr(ex), _ptr(am))
+        return r, dn, ex, am
+
+    def state(self):
+        out = np.empty((self.b.K, 16), np.int64)
+        self.lib.oracle_env_get(self.b.ctx, self.env, _ptr(out))
         return out

@@ -30,6 +30,7 @@
  * closed forms, inline invariants).  Every function below is pinned; none is
  * "parity unpinned".
  */
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -488,4 +489,171 @@ void oracle_get_stats(oracle_ctx *X, int64_t *out) {
 }
 void oracle_get_violations(oracle_ctx *X, int64_t *out) {
     for (int k = 0; k < X->K; k++) out[k] = X->books[k].violations;
+}
+
+/* ===================================================================== */
+/* NEXT row N3: the execution-environment step (Sec.5.1.3 and 5.2), one env
+ * per book.  Written in the order of the paper's step:
+ *   1. the agent's action becomes messages: cancel the agent's orders of
+ *      the previous step, then either the forced market order for the remaining
+ *      task one minute before the episode ends or one limit order per
+ *      positive size at the far-touch, mid, near-touch and passive prices
+ *      (P:L476-493);
+ *   2. the step's data messages follow -- one trade log for the step (G9);
+ *   3. the current time becomes the last data message's time;
+ *   4. reward (eq:rewardfunc, N2) and the executed quantity from the agent's trades;
+ *   5. done when the task is complete or the episode time is over
+ *      (P:L423).  Readings E1-E8 are listed in DESIGN.md. */
+typedef struct {
+    int32_t task_side;   /* -1 sell, +1 buy */
+    int32_t task_size;
+    int32_t n_passive;   /* ticks behind the near touch for the passive price */
+    int32_t tick;
+    int32_t episode_s;
+    int32_t agent_tid;
+    int32_t oid_base;    /* agent OIDs are oid_base, oid_base+1, ... (E4) */
+    int32_t pad;
+    double lambda;
+} env_cfg;
+
+typedef struct {
+    int64_t executed;
+    int32_t init_ts, init_tns, cur_ts, cur_tns, next_oid, done, last_ask, last_bid;
+    int32_t live[4];
+    double p_init;
+} oenv;
+
+static int32_t best_price_of(oracle_ctx *X, const obook *b, int ask) {
+    int32_t o[4];
+    l2_levels(X, b, o, 1);
+    return ask ? o[0] : o[2];
+}
+
+void *oracle_env_create(int32_t K) { return calloc((size_t)(K > 0 ? K : 1), sizeof(oenv)); }
+void oracle_env_destroy(void *e) { free(e); }
+
+/* after oracle_init: P_init = the mid price (P_ask + P_bid)/2 of the initial book */
+void oracle_env_reset(oracle_ctx *X, void *envp, const env_cfg *c, int32_t init_ts, int32_t init_tns) {
+    oenv *E = (oenv *)envp;
+    for (int k = 0; k < X->K; k++) {
+        oenv *e = &E[k];
+        memset(e, 0, sizeof *e);
+        e->init_ts = e->cur_ts = init_ts;
+        e->init_tns = e->cur_tns = init_tns;
+        e->next_oid = c->oid_base;
+        e->last_ask = best_price_of(X, &X->books[k], 1);
+        e->last_bid = best_price_of(X, &X->books[k], 0);
+        /* E7: a one-sided initial book takes the price of the side that exists */
+        int32_t a = e->last_ask > 0 ? e->last_ask : e->last_bid, bq = e->last_bid > 0 ? e->last_bid : e->last_ask;
+        e->p_init = (a > 0) ? ((double)a + (double)bq) / 2.0 : 0.0;
+    }
+}
+
+static int64_t elapsed_ns(const oenv *e) {
+    return ((int64_t)e->cur_ts - e->init_ts) * 1000000000LL + ((int64_t)e->cur_tns - e->init_tns);
+}
+
+/* The agent's messages of one step for one env (at most 8; unused rows stay zero):
+ * exposed so tests can check the action mapping on its own. */
+static void env_agent_msgs(oracle_ctx *X, const obook *b, oenv *e, const env_cfg *c, const float *a,
+                           int32_t *m /*[8][8]*/) {
+    memset(m, 0, 8 * 8 * sizeof(int32_t));
+    if (e->done) return;
+    int n = 0;
+    int32_t S = c->task_side;
+    for (int i = 0; i < 4; i++)                                   /* E1: cancel the previous orders */
+        if (e->live[i] != 0) {
+            int32_t *r = m + 8 * n++;
+            r[0] = 3; r[1] = S; r[2] = 2147483647; r[3] = 0; r[4] = e->live[i]; r[5] = c->agent_tid;
+            r[6] = e->cur_ts; r[7] = e->cur_tns;
+            e->live[i] = 0;
+        }
+    int64_t remaining = (int64_t)c->task_size - e->executed;
+    if (remaining <= 0) return;
+    if (elapsed_ns(e) >= ((int64_t)c->episode_s - 60) * 1000000000LL) {   /* forced market order */
+        int32_t *r = m + 8 * n++;
+        r[0] = 4; r[1] = S; r[2] = (int32_t)(remaining > 2147483647 ? 2147483647 : remaining); r[3] = 0;
+        r[4] = e->next_oid++; r[5] = c->agent_tid; r[6] = e->cur_ts; r[7] = e->cur_tns;
+        return;
+    }
+    /* prices from the current book; an empty side keeps its last valid price (E6) */
+    int32_t ask = best_price_of(X, b, 1), bid = best_price_of(X, b, 0);
+    if (ask > 0) e->last_ask = ask; else ask = e->last_ask;
+    if (bid > 0) e->last_bid = bid; else bid = e->last_bid;
+    int32_t far = (S == -1) ? bid : ask;
+    int32_t near = (S == -1) ? ask : bid;
+    int32_t passive = (near > 0) ? near - S * c->n_passive * c->tick : 0;
+    int32_t mid = 0;                                                      /* P:L449, E5 */
+    if (ask > 0 && bid > 0) {
+        int64_t twice = (int64_t)ask + bid, t2 = 2LL * c->tick;
+        int64_t q = twice / t2, rmd = twice % t2;
+        mid = (int32_t)((S == -1 && rmd) ? (q + 1) * c->tick : q * c->tick);
+    }
+    int32_t price[4] = {far, mid, near, passive};
+    int li = 0;
+    for (int k = 0; k < 4; k++) {
+        float x = a[k];
+        int64_t q = 0;                                                    /* E2: rint, NaN/negative -> 0 */
+        if (x == x && x > 0.0f) q = (x >= 2147483647.0f) ? 2147483647LL : (int64_t)rintf(x);
+        if (q > remaining) q = remaining;                                 /* E3: far touch first */
+        if (q <= 0 || price[k] <= 0) continue;
+        remaining -= q;
+        int32_t *r = m + 8 * n++;
+        r[0] = 1; r[1] = S; r[2] = (int32_t)q; r[3] = price[k]; r[4] = e->next_oid; r[5] = c->agent_tid;
+        r[6] = e->cur_ts; r[7] = e->cur_tns;
+        e->live[li++] = e->next_oid++;
+    }
+}
+
+void oracle_env_step(oracle_ctx *X, void *envp, const env_cfg *c, const float *actions /*[K][4]*/,
+                     const int32_t *data /*[K][M][8]*/, int32_t M, double *reward, int32_t *done,
+                     int64_t *executed, int32_t *agent_out /*[K][8][8] or NULL*/) {
+    oenv *E = (oenv *)envp;
+    int32_t *stream = (int32_t *)malloc(sizeof(int32_t) * (size_t)(8 + M) * 8);
+    for (int k = 0; k < X->K; k++) {
+        oenv *e = &E[k];
+        obook *b = &X->books[k];
+        int was_done = e->done;
+        env_agent_msgs(X, b, e, c, actions + 4 * k, stream);
+        if (agent_out) memcpy(agent_out + (size_t)k * 64, stream, 64 * sizeof(int32_t));
+        /* E8: a finished env receives only padding (T = 0) messages: its book does not
+         * change; the padding is counted and the trade log cleared like any call */
+        if (was_done) memset(stream + 64, 0, sizeof(int32_t) * (size_t)M * 8);
+        else memcpy(stream + 64, data + (size_t)k * M * 8, sizeof(int32_t) * (size_t)M * 8);
+        /* one call of 8 + M messages: the trade log is the step's (G9) */
+        for (int i = 0; i < X->T_cap; i++) for (int f = 0; f < T_NF; f++) b->trades[(size_t)i * T_NF + f] = -1;
+        b->n_trades = 0;
+        for (int i = 0; i < 8 + M; i++) process(X, b, stream + (size_t)i * M_NF);
+        if (was_done) { reward[k] = 0.0; done[k] = 1; executed[k] = e->executed; continue; }
+        int32_t agent[2] = {c->oid_base, e->next_oid - 1};
+        double r, v;
+        int64_t qa;
+        oracle_ctx one = *X;                                              /* reward over this book only */
+        one.K = 1;
+        one.books = b;
+        oracle_step_reward(&one, agent, &e->p_init, &c->task_side, c->lambda, &r, &v, &qa);
+        e->executed += qa;
+        for (int i = M - 1; i >= 0; i--) {
+            const int32_t *d = data + ((size_t)k * M + i) * 8;
+            if (d[0] != 0) { e->cur_ts = d[6]; e->cur_tns = d[7]; break; }
+        }
+        e->done = (e->executed >= c->task_size) || (elapsed_ns(e) > (int64_t)c->episode_s * 1000000000LL);
+        reward[k] = r; done[k] = e->done; executed[k] = e->executed;
+    }
+    free(stream);
+}
+
+/* env state export: [K][16] int64 = executed, init ts/tns, cur ts/tns, next_oid, done,
+ * last_ask, last_bid, live[4], p_init bits, 0 */
+void oracle_env_get(oracle_ctx *X, void *envp, int64_t *out) {
+    oenv *E = (oenv *)envp;
+    for (int k = 0; k < X->K; k++) {
+        oenv *e = &E[k];
+        int64_t *o = out + (size_t)k * 16;
+        o[0] = e->executed; o[1] = e->init_ts; o[2] = e->init_tns; o[3] = e->cur_ts; o[4] = e->cur_tns;
+        o[5] = e->next_oid; o[6] = e->done; o[7] = e->last_ask; o[8] = e->last_bid;
+        for (int i = 0; i < 4; i++) o[9 + i] = e->live[i];
+        memcpy(&o[13], &e->p_init, sizeof(double));
+        o[14] = o[15] = 0;
+    }
 }
