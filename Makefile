@@ -9,7 +9,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xptxas -
 PKG       := paper_2308_13289_b200
 LIB       := $(PKG)/liblob.so
 SRCS      := $(PKG)/csrc/lob_api.cu
-DEPS      := $(SRCS) $(PKG)/csrc/lob_kernels.cuh include/lob.h
+DEPS      := $(SRCS) $(PKG)/csrc/lob_kernels.cuh $(PKG)/csrc/lob_env.cuh include/lob.h
 
 all: $(LIB) $(PKG)/liblobster.so oracle/liblob_oracle.so lobgen/liblobgen.so
 

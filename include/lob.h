@@ -143,6 +143,41 @@ int lob_step_reward(lob_ctx *ctx, const int32_t *d_agent_oids, const double *d_p
                     const int32_t *d_task_side, double lambda, double *d_reward, double *d_vwap,
                     int64_t *d_agent_qty, void *cuda_stream);
 
+/* NEXT row N3: the execution-environment step on the device, one
+ * env per book (Sec.5.1.3 and 5.2; readings E1-E8 in DESIGN.md). */
+typedef struct {
+    int32_t task_side;      /* -1 sell task, +1 buy task                               */
+    int32_t task_size;      /* shares to execute (> 0)                                 */
+    int32_t n_passive;      /* passive price = near touch -/+ n ticks      */
+    int32_t tick;           /* price tick (> 0)                                        */
+    int32_t episode_s;      /* episode length in seconds; forced market order
+                               for the remaining task 60 s before the end      */
+    int32_t agent_tid;      /* TID stamped on the agent's orders                        */
+    int32_t agent_oid_base; /* the agent's OIDs are base, base+1, ... (G29)            */
+    int32_t reserved;
+    double lambda;          /* drift weight of eq:rewardfunc               */
+} lob_env_config;
+
+/* Bytes of env state for n_envs envs (caller-allocated device memory, 16-byte aligned). */
+size_t lob_env_state_bytes(int32_t n_envs);
+
+/* After lob_init: start an episode in every book: P_init = (best ask + best bid)/2
+ * of the current book, time = (init_ts, init_tns), executed = 0. */
+int lob_env_reset(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, int32_t init_ts,
+                  int32_t init_tns, void *cuda_stream);
+
+/* One env step in every book (3 kernel launches on cuda_stream):
+ *  d_actions [K][4] f32: sizes at the far-touch, mid, near-touch and passive prices
+ *  (P:L476-493), rounded half-even, negative/NaN -> 0, capped far-touch first by the
+ *  remaining task; d_data [K][msgs_per_step][8]: the step's data messages (zero rows
+ *  are padding, G21); d_work [K][8+msgs_per_step][8] int32 workspace that receives the
+ *  step's stream (rows 0..7 the agent's messages, zero-padded); outputs (nullable):
+ *  d_reward [K] f64 (eq:rewardfunc), d_done [K] int32, d_executed [K] int64, and the
+ *  post-step L2 d_l2_out [K][1][L][4].  A finished env receives padding only. */
+int lob_env_step(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const float *d_actions,
+                 const int32_t *d_data, int32_t msgs_per_step, int32_t *d_work, double *d_reward,
+                 int32_t *d_done, int64_t *d_executed, int32_t *d_l2_out, void *cuda_stream);
+
 /* Current L2 snapshot of every book: d_out [K][L][4] int32. */
 int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *cuda_stream);
 

@@ -4,8 +4,8 @@ arXiv 2308.13289, Section 4).
 The product is ``liblob.so`` behind the C ABI in ``include/lob.h``; this package is
 its thin binding.  See DESIGN.md.
 """
-from .lob import (LIB_PATH, LOB_NSTATS, MAX_CAPACITY, MAX_L2_LEVELS, STAT_NAMES, LobBatch,
-                  LobError, launch_count, lib)
+from .lob import (LIB_PATH, LOB_NSTATS, MAX_CAPACITY, MAX_L2_LEVELS, STAT_NAMES, EnvConfig, LobBatch,
+                  LobEnv, LobError, launch_count, lib)
 
-__all__ = ["LobBatch", "LobError", "lib", "launch_count", "LIB_PATH", "LOB_NSTATS",
+__all__ = ["LobBatch", "LobEnv", "EnvConfig", "LobError", "lib", "launch_count", "LIB_PATH", "LOB_NSTATS",
            "STAT_NAMES", "MAX_CAPACITY", "MAX_L2_LEVELS"]

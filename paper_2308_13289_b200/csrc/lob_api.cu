@@ -11,11 +11,13 @@
 
 #include "../../include/lob.h"
 #include "lob_kernels.cuh"
+#include "lob_env.cuh"
 
 using namespace lobk;
 
 static_assert((int)NST == (int)LOB_NSTATS, "counter layout");
 static_assert(F_P == 0 && F_TNS == 5, "field order");
+static_assert(sizeof(lob_env_config) == sizeof(EnvCfg), "env config layout");
 
 namespace {
 thread_local char g_err[512] = "";
@@ -324,6 +326,59 @@ int lob_step_reward(lob_ctx *ctx, const int32_t *d_agent_oids, const double *d_p
         ctx->trades(), ctx->ntr(), K, ctx->cfg.trades_cap, d_agent_oids, d_p_init, d_task_side, lambda, d_reward,
         d_vwap, reinterpret_cast<long long *>(d_agent_qty));
     return after_launch("lob_reward_kernel");
+}
+
+size_t lob_env_state_bytes(int32_t n_envs) { return n_envs < 0 ? 0 : (size_t)n_envs * sizeof(EnvState); }
+
+static int env_cfg_ok(const lob_env_config *c) {
+    return c && (c->task_side == 1 || c->task_side == -1) && c->task_size > 0 && c->tick > 0 && c->n_passive >= 0 &&
+           c->episode_s > 0;
+}
+
+int lob_env_reset(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, int32_t init_ts, int32_t init_tns,
+                  void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (!env_cfg_ok(cfg)) return fail(LOB_EINVAL, "invalid lob_env_config%s");
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    if (!d_env || reinterpret_cast<uintptr_t>(d_env) % 16) return fail(LOB_EINVAL, "d_env null or misaligned%s");
+    EnvCfg c;
+    memcpy(&c, cfg, sizeof c);
+    lob_env_reset_kernel<<<blocks_for(K, 8), 256, 0, (cudaStream_t)stream>>>(
+        ctx->book(), ctx->cfg.capacity, ctx->lay.NP, K, static_cast<EnvState *>(d_env), c, init_ts, init_tns);
+    return after_launch("lob_env_reset_kernel");
+}
+
+int lob_env_step(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const float *d_actions,
+                 const int32_t *d_data, int32_t msgs_per_step, int32_t *d_work, double *d_reward, int32_t *d_done,
+                 int64_t *d_executed, int32_t *d_l2_out, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (!env_cfg_ok(cfg)) return fail(LOB_EINVAL, "invalid lob_env_config%s");
+    if (msgs_per_step < 0 || msgs_per_step > (1 << 24)) return fail(LOB_EINVAL, "bad msgs_per_step%s");
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    if (!d_env || !d_actions || !d_work || (msgs_per_step > 0 && !d_data))
+        return fail(LOB_EINVAL, "env, actions, work and data buffers are required%s");
+    if (reinterpret_cast<uintptr_t>(d_env) % 16 || reinterpret_cast<uintptr_t>(d_work) % 16 ||
+        reinterpret_cast<uintptr_t>(d_data) % 16 || reinterpret_cast<uintptr_t>(d_l2_out) % 16 ||
+        reinterpret_cast<uintptr_t>(d_reward) % 8 || reinterpret_cast<uintptr_t>(d_executed) % 8)
+        return fail(LOB_EINVAL, "misaligned buffer%s");
+    EnvCfg c;
+    memcpy(&c, cfg, sizeof c);
+    cudaStream_t st = (cudaStream_t)stream;
+    EnvState *env = static_cast<EnvState *>(d_env);
+    lob_env_actions_kernel<<<blocks_for(K, 8), 256, 0, st>>>(ctx->book(), ctx->cfg.capacity, ctx->lay.NP, K, env, c,
+                                                             d_actions, d_data, msgs_per_step, d_work);
+    rc = after_launch("lob_env_actions_kernel");
+    if (rc) return rc;
+    rc = launch_step(ctx, d_work, 1, 8 + msgs_per_step, d_l2_out, 0, K, st);
+    if (rc) return rc;
+    lob_env_post_kernel<<<blocks_for(K, 8), 256, 0, st>>>(ctx->trades(), ctx->ntr(), ctx->cfg.trades_cap, K, env, c,
+                                                          d_data, msgs_per_step, d_reward, d_done,
+                                                          reinterpret_cast<long long *>(d_executed));
+    return after_launch("lob_env_post_kernel");
 }
 
 int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *stream) {

@@ -36,6 +36,13 @@ class _Config(ctypes.Structure):
                 ("device", ctypes.c_int32)]
 
 
+class EnvConfig(ctypes.Structure):
+    """lob_env_config (include/lob.h): the execution task shared by all envs (NEXT row N3)."""
+    _fields_ = [("task_side", ctypes.c_int32), ("task_size", ctypes.c_int32), ("n_passive", ctypes.c_int32),
+                ("tick", ctypes.c_int32), ("episode_s", ctypes.c_int32), ("agent_tid", ctypes.c_int32),
+                ("agent_oid_base", ctypes.c_int32), ("reserved", ctypes.c_int32), ("lam", ctypes.c_double)]
+
+
 def lib():
     """Load liblob.so (built by ``make`` / ``__graft_entry__.build()``); raise if absent."""
     global _lib
@@ -68,6 +75,13 @@ def lib():
             if hasattr(L, "lob_step_reward"):
                 L.lob_step_reward.restype = ctypes.c_int
                 L.lob_step_reward.argtypes = [P, P, P, P, ctypes.c_double, P, P, P, P]
+            if hasattr(L, "lob_env_step"):
+                L.lob_env_state_bytes.restype = ctypes.c_size_t
+                L.lob_env_state_bytes.argtypes = [i32]
+                L.lob_env_reset.restype = ctypes.c_int
+                L.lob_env_reset.argtypes = [P, P, ctypes.POINTER(EnvConfig), i32, i32, P]
+                L.lob_env_step.restype = ctypes.c_int
+                L.lob_env_step.argtypes = [P, P, ctypes.POINTER(EnvConfig), P, P, i32, P, P, P, P, P, P]
             L.lob_launch_count.restype = ctypes.c_int64
             L.lob_strerror.restype = ctypes.c_char_p
             L.lob_strerror.argtypes = [ctypes.c_int]
@@ -233,3 +247,36 @@ class LobBatch:
         with torch.cuda.device(self.device):
             _check(lib().lob_get_stats(self.ctx, _ptr(out), _stream(stream)), "lob_get_stats")
         return out
+
+
+class LobEnv:
+    """Execution environments on the device, one per book of a LobBatch (NEXT row N3):
+    lob_env_reset / lob_env_step (Sec.5.1.3 and 5.2)."""
+
+    def __init__(self, batch: LobBatch, config: EnvConfig, msgs_per_step: int):
+        self.b, self.cfg, self.M = batch, config, int(msgs_per_step)
+        L = lib()
+        n = L.lob_env_state_bytes(batch.K)
+        self.state = torch.empty(max(int(n), 64), dtype=torch.uint8, device=batch.device)
+        self.work = torch.empty((batch.K, 8 + self.M, 8), dtype=torch.int32, device=batch.device)
+        self.reward = torch.empty((batch.K,), dtype=torch.float64, device=batch.device)
+        self.done = torch.empty((batch.K,), dtype=torch.int32, device=batch.device)
+        self.executed = torch.empty((batch.K,), dtype=torch.int64, device=batch.device)
+
+    def reset(self, init_ts: int, init_tns: int = 0, stream=None):
+        with torch.cuda.device(self.b.device):
+            _check(lib().lob_env_reset(self.b.ctx, _ptr(self.state), ctypes.byref(self.cfg), int(init_ts),
+                                       int(init_tns), _stream(stream)), "lob_env_reset")
+
+    def step(self, actions, data, l2_out=None, stream=None):
+        """actions [K][4] f32, data [K][M][8] int32 -> (reward, done, executed) device tensors;
+        ``self.work[:, :8]`` holds the agent's messages of the step."""
+        a = self.b._dev(actions, torch.float32)
+        d = self.b._dev(data)
+        assert a.shape == (self.b.K, 4) and d.shape == (self.b.K, self.M, 8)
+        with torch.cuda.device(self.b.device):
+            _check(lib().lob_env_step(self.b.ctx, _ptr(self.state), ctypes.byref(self.cfg), _ptr(a), _ptr(d),
+                                      self.M, _ptr(self.work), _ptr(self.reward), _ptr(self.done),
+                                      _ptr(self.executed), _ptr(l2_out), _stream(stream)), "lob_env_step")
+        self._keep = (a, d)
+        return self.reward, self.done, self.executed

@@ -246,3 +246,71 @@ def test_lobster_windows_end_to_end(tmp_path):
         res.append((e.process(w.msgs, w.n_steps, w.msgs_per_step), e.book(), e.stats()))
     for a, b in zip(*res):
         np.testing.assert_array_equal(a, b)
+
+
+# ------------------------------------------- NEXT row N3: execution-env step on device
+def _env_pair(K, N, cfg_kw, init, Tcap=512, L=10):
+    from paper_2308_13289_b200 import EnvConfig, LobEnv
+    ge = GpuEngine(K, N, Tcap, L)
+    oe = oracle.OracleBatch(K, N, Tcap, L)
+    for e in (ge, oe):
+        e.init(init, lobgen.INIT_TS, lobgen.INIT_TNS)
+    gcfg = EnvConfig(**cfg_kw)
+    ocfg = oracle.EnvConfig(cfg_kw["task_side"], cfg_kw["task_size"], cfg_kw["n_passive"], cfg_kw["tick"],
+                            cfg_kw["episode_s"], cfg_kw["agent_tid"], cfg_kw["agent_oid_base"], 0, cfg_kw["lam"])
+    return ge, oe, gcfg, ocfg, LobEnv
+
+
+def test_env_golden_on_gpu():
+    """The hand-derived N3 traces of tests/test_env_pins.py, on the device."""
+    from test_env_pins import BASE, DATA1, INIT, NONE
+    kw = dict(task_side=-1, task_size=10, n_passive=2, tick=10, episode_s=61, agent_tid=77,
+              agent_oid_base=BASE, reserved=0, lam=1.0)
+    from paper_2308_13289_b200 import EnvConfig, LobBatch, LobEnv
+    b = LobBatch(1, 8, 16, 2)
+    b.init(torch.from_numpy(INIT), 34200, 0)
+    env = LobEnv(b, EnvConfig(**kw), 1)
+    env.reset(34200, 0)
+    r, d, x = env.step(np.array([[2.4, 1.6, 3.5, 0.5]], np.float32), DATA1)
+    assert r.item() == -20.0 and x.item() == 4 and d.item() == 0
+    np.testing.assert_array_equal(env.work[0, :3].cpu().numpy(), [[1, -1, 2, 990, BASE, 77, 34200, 0],
+                                                                  [1, -1, 2, 1000, BASE + 1, 77, 34200, 0],
+                                                                  [1, -1, 4, 1010, BASE + 2, 77, 34200, 0]])
+    r, d, x = env.step(np.array([[9, 9, 9, 9]], np.float32), NONE)
+    assert abs(r.item() + 65.0) < 1e-9 and x.item() == 10 and d.item() == 1
+    assert env.work[0, 3].cpu().tolist() == [4, -1, 6, 0, BASE + 3, 77, 34201, 0]
+
+
+@pytest.mark.parametrize("K,N,side,episode", [(1000, 100, -1, 1800), (500, 100, 1, 40), (64, 512, -1, 600),
+                                               (24, 2048, 1, 600)])
+def test_env_rollout_parity(K, N, side, episode):
+    """Random actions over 12 steps of 100 data messages (the RL shape):
+    agent messages, books, executed quantities and done flags bit-exact; rewards within
+    1e-12 of the magnitude of their terms."""
+    cfg = lobgen.Config("env", K, N, 12, 100, min(N // 3, 33), 512, 10, "lobster", 40 + K)
+    msgs, init = lobgen.generate(cfg)
+    kw = dict(task_side=side, task_size=3000, n_passive=2, tick=100, episode_s=episode, agent_tid=77,
+              agent_oid_base=2_000_000_000, reserved=0, lam=0.5)
+    ge, oe, gcfg, ocfg, LobEnv = _env_pair(K, N, kw, init)
+    genv = LobEnv(ge.b, gcfg, 100)
+    oenv = oracle.OracleEnv(oe, ocfg)
+    genv.reset(lobgen.INIT_TS, lobgen.INIT_TNS)
+    oenv.reset(lobgen.INIT_TS, lobgen.INIT_TNS)
+    rng = np.random.default_rng(K)
+    prev = np.zeros(K, np.int64)
+    for s in range(cfg.n_steps):
+        acts = rng.uniform(-100, 600, (K, 4)).astype(np.float32)
+        acts[rng.random((K, 4)) < 0.03] = np.nan
+        data = np.ascontiguousarray(msgs[:, s * 100:(s + 1) * 100])
+        r, d, x = genv.step(torch.from_numpy(acts), torch.from_numpy(data))
+        ro, do, xo, am = oenv.step(acts, data, 100)
+        np.testing.assert_array_equal(genv.work[:, :8].cpu().numpy(), am, err_msg=f"agent msgs step {s}")
+        np.testing.assert_array_equal(d.cpu().numpy(), do)
+        np.testing.assert_array_equal(x.cpu().numpy(), xo)
+        rg = r.cpu().numpy()
+        # magnitude of eq:rewardfunc's terms: sum_j Q_j (|P_j| + |VWAP|) (1 + lambda), prices < 2e6
+        scale = (xo - prev).astype(np.float64) * 4e6 * (1 + kw["lam"])
+        prev = xo.copy()
+        assert np.all(np.abs(rg - ro) <= 1e-12 * np.maximum(1.0, scale)), (s, np.abs(rg - ro).max())
+        np.testing.assert_array_equal(ge.book(), oe.book())
+        np.testing.assert_array_equal(ge.stats(), oe.stats())
