@@ -203,10 +203,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; LOB_DIST_BACKEND=gloo lets several ranks share one GPU to
+    # exercise the multi-rank logic on a single-GPU box (NCCL refuses shared GPUs)
+    backend = os.environ.get("LOB_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = lobgen.CONFIGS[args.config]
     book0, K = shard_books(rank, world, cfg.n_books, args.scaling)
     cfg = cfg.with_(n_books=K)

@@ -34,11 +34,16 @@ def _active():
     return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
 
 
+def _coll_device(device):
+    """NCCL reduces device tensors; gloo (CPU tests, single-GPU multi-rank checks) host tensors."""
+    return device if dist.get_backend() == "nccl" else "cpu"
+
+
 def reduce_max(value: float, device=None) -> float:
     """Max over ranks (the timing rule: a multi-GPU time is the slowest rank's)."""
     if not _active():
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -46,7 +51,7 @@ def reduce_max(value: float, device=None) -> float:
 def reduce_sum(value: int, device=None) -> int:
     if not _active():
         return int(value)
-    t = torch.tensor([int(value)], dtype=torch.int64, device=device)
+    t = torch.tensor([int(value)], dtype=torch.int64, device=_coll_device(device))
     dist.all_reduce(t)
     return int(t.item())
 
@@ -55,6 +60,8 @@ def gather_rows(local: torch.Tensor) -> torch.Tensor:
     """Concatenate every rank's [n_i, ...] tensor in rank order (variable n_i allowed)."""
     if not _active():
         return local
+    if dist.get_backend() != "nccl" and local.is_cuda:
+        return gather_rows(local.cpu()).to(local.device)
     world = dist.get_world_size()
     n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
