@@ -164,13 +164,16 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- CPU baseline leg
-def cpu_baseline(cfg, msgs_h, init_h, seconds, gpu_stats_h):
+def cpu_baseline(cfg, msgs_h, init_h, seconds, gpu):
     """The oracle as it stands, on the host cores, over a bounded sample of the same
-    workload (leading books, growing until ~`seconds` of CPU time)."""
+    workload (leading books, growing until ~`seconds` of CPU time).  The oracle's
+    outputs for the sampled books are then compared with the GPU's (`gpu`: host copies
+    of the exported book, trade log, trade counts, per-step L2 and counters), so every
+    bench run is also a full-size parity check on the sample (outside the timed region)."""
     import oracle
     cores = len(os.sched_getaffinity(0))
     nb, done_books, total = 512, 0, 0.0
-    match = True
+    mism = set()
     while total < seconds and done_books < cfg.n_books:
         n = min(nb, cfg.n_books - done_books)
         sl = slice(done_books, done_books + n)
@@ -179,16 +182,20 @@ def cpu_baseline(cfg, msgs_h, init_h, seconds, gpu_stats_h):
         i = np.ascontiguousarray(init_h[sl])
         t0 = time.perf_counter()
         o.init(i, lobgen.INIT_TS, lobgen.INIT_TNS)
-        o.process(m, cfg.n_steps, cfg.msgs_per_step)
+        l2 = o.process(m, cfg.n_steps, cfg.msgs_per_step)
         total += time.perf_counter() - t0
-        match = match and np.array_equal(o.stats(), gpu_stats_h[sl])
+        tr, cnt = o.trades()
+        for key, want in (("stats", o.stats()), ("book", o.book()), ("trades", tr), ("n_trades", cnt), ("l2", l2)):
+            if not np.array_equal(want, gpu[key][sl]):
+                mism.add(key)
         done_books += n
         nb *= 2
     v = done_books * cfg.n_msgs / total
     return {"value": v, "unit": "msg/s", "cores": cores, "kind": "oracle",
             "sample": f"first {done_books} of {cfg.n_books} books of {cfg.name} "
                       f"({done_books * cfg.n_msgs} messages, {total:.1f} s wall on {cores} threads over books)",
-            "counters_match_gpu": bool(match)}
+            "parity": {"books": done_books, "outputs": ["book", "trades", "n_trades", "l2", "stats"],
+                       "bit_exact": not mism, "mismatched": sorted(mism)}}
 
 
 # ------------------------------------------------------------------------ our arm
@@ -266,9 +273,16 @@ def main():
     st = b.stats()
     _, ntr = b.trades()
     trades_logged = int(ntr.sum().item())
-    allst = gather_rows(st)                                     # NCCL gather of per-book counters
+    # NCCL gather of per-book counters + state digests (lob_digest)
+    allst = gather_rows(torch.cat([st, b.digest()[:, None]], 1))
     trades_total = reduce_sum(trades_logged, dev)
-    stats_sum = allst.sum(0).cpu().tolist()
+    stats_sum = allst[:, :10].sum(0).cpu().tolist()
+    dg = allst[:, 10].cpu().numpy().view(np.uint64)
+    # xor-folds: over every book, and over global books [0, K) -- the latter is the same at
+    # every world size (each book's stream depends only on its global id)
+    digest = {"all_books": "%016x" % int(np.bitwise_xor.reduce(dg)),
+              "first_books": "%016x" % int(np.bitwise_xor.reduce(dg[:cfg.n_books])),
+              "first_books_n": cfg.n_books}
     total_books = reduce_sum(K, dev)
 
     total_msgs = total_books * cfg.n_msgs * args.steps
@@ -340,7 +354,12 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, msgs_h.numpy(), init_h.numpy(), args.cpu_seconds, st.cpu().numpy())
+        tr_d, cnt_d = b.trades()
+        gpu = {"stats": st.cpu().numpy(), "book": b.book().cpu().numpy(), "trades": tr_d.cpu().numpy(),
+               "n_trades": cnt_d.cpu().numpy(), "l2": l2_d.cpu().numpy()}
+        del tr_d
+        cpu = cpu_baseline(cfg, msgs_h.numpy(), init_h.numpy(), args.cpu_seconds, gpu)
+        del gpu
 
     if rank == 0:
         line = {"metric": "messages/sec", "value": value, "unit": "msg/s", "n_gpus": world, "steps": args.steps,
@@ -354,7 +373,7 @@ def main():
                            "l2_flush": "inputs larger than L2 (messages %.2f GB/GPU > 126 MB)"
                                        % (msgs_h.numel() * 4 / 1e9)},
                 "roofline": roofline, "roofline_issue": roofline_issue, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": n_launch,
+                "gpu_launches": n_launch, "digest": digest,
                 "clocks": sampler.summary(),
                 "totals": dict(zip(["msgs", "bad", "trades", "trades_dropped", "traded_qty", "cancelled_qty",
                                     "unknown_cancels", "add_overflow", "overflow_qty", "market_discarded_qty"],

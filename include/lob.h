@@ -192,6 +192,16 @@ int lob_get_book(lob_ctx *ctx, int32_t *d_out, void *cuda_stream);
 /* Counters: d_out [K][LOB_NSTATS] int64. */
 int lob_get_stats(lob_ctx *ctx, int64_t *d_out, void *cuda_stream);
 
+/* Per-book state digest (the full-state fingerprint that lets ranks and
+ * world sizes be compared without moving the state).  d_out [K] uint64: FNV-1a-64
+ * (offset basis 0xcbf29ce484222325, prime 0x100000001b3) over the little-endian bytes of,
+ * in order, the book as lob_get_book exports it ([2][N][6] int32, empty slots -1), the
+ * trade log as lob_get_trades exports it ([trades_cap][6] int32, -1 tail), n_trades
+ * (int32) and the counters ([LOB_NSTATS] int64).  Equal digests <=> (up to hash
+ * collisions) identical observable state.  Off the hot path: one thread per book.
+ * Errors: LOB_EINVAL for a null d_out with K > 0. */
+int lob_digest(lob_ctx *ctx, uint64_t *d_out, void *cuda_stream);
+
 /* Number of kernels this process has launched through the library (all contexts). */
 int64_t lob_launch_count(void);
 

@@ -431,6 +431,18 @@ int lob_get_stats(lob_ctx *ctx, int64_t *d_out, void *stream) {
     return e == cudaSuccess ? LOB_OK : cuda_fail(e, "lob_get_stats copy");
 }
 
+int lob_digest(lob_ctx *ctx, uint64_t *d_out, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return LOB_OK;
+    if (!d_out) return fail(LOB_EINVAL, "d_out is null%s");
+    lob_digest_kernel<<<blocks_for(K, 128), 128, 0, (cudaStream_t)stream>>>(
+        ctx->book(), ctx->trades(), ctx->ntr(), ctx->stats(), reinterpret_cast<unsigned long long *>(d_out), K,
+        ctx->cfg.capacity, ctx->lay.NP, ctx->cfg.trades_cap);
+    return after_launch("lob_digest_kernel");
+}
+
 int64_t lob_launch_count(void) { return g_launches.load(); }
 
 const char *lob_strerror(int code) {

@@ -802,6 +802,42 @@ __global__ void lob_export_trades(const int32_t *trades, const int32_t *ntrades,
     if (counts && t < K) counts[t] = ntrades[t];
 }
 
+// per-book FNV-1a-64 over the exported state (include/lob.h lob_digest): one thread per book
+__device__ __forceinline__ unsigned long long fnv1a_word(unsigned long long h, uint32_t w) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        h ^= (w >> (8 * k)) & 0xffu;
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+__global__ void lob_digest_kernel(const int32_t *book, const int32_t *trades, const int32_t *ntrades,
+                                  const long long *stats, unsigned long long *out, int K, int N, int NP, int Tcap) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= K) return;
+    unsigned long long h = 0xcbf29ce484222325ULL;
+    const int32_t *bk = book + (size_t)b * 2 * NF * NP;
+    for (int s = 0; s < 2; ++s)
+        for (int i = 0; i < N; ++i) {
+            const int32_t *src = bk + s * NF * NP + i;
+            const bool occ = src[F_Q * NP] > 0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) h = fnv1a_word(h, occ ? (uint32_t)src[f * NP] : 0xffffffffu);
+        }
+    const int nt = ntrades[b];
+    const int32_t *tr = trades + (size_t)b * Tcap * 6;
+    for (int r = 0; r < Tcap; ++r)
+#pragma unroll
+        for (int f = 0; f < 6; ++f) h = fnv1a_word(h, r < nt ? (uint32_t)tr[r * 6 + f] : 0xffffffffu);
+    h = fnv1a_word(h, (uint32_t)nt);
+    for (int c = 0; c < NST; ++c) {
+        const unsigned long long v = (unsigned long long)stats[(size_t)b * NST + c];
+        h = fnv1a_word(fnv1a_word(h, (uint32_t)v), (uint32_t)(v >> 32));
+    }
+    out[b] = h;
+}
+
 // current L2 of every book from the stored state: one group per book (G = 1)
 template <int KPL, int W>
 __global__ void __launch_bounds__(32 * W) lob_export_l2(const int32_t *book, int32_t *out, int K, int N, int L) {

@@ -82,6 +82,9 @@ def lib():
                 L.lob_env_reset.argtypes = [P, P, ctypes.POINTER(EnvConfig), i32, i32, P]
                 L.lob_env_step.restype = ctypes.c_int
                 L.lob_env_step.argtypes = [P, P, ctypes.POINTER(EnvConfig), P, P, i32, P, P, P, P, P, P]
+            if hasattr(L, "lob_digest"):
+                L.lob_digest.restype = ctypes.c_int
+                L.lob_digest.argtypes = [P, P, P]
             L.lob_launch_count.restype = ctypes.c_int64
             L.lob_strerror.restype = ctypes.c_char_p
             L.lob_strerror.argtypes = [ctypes.c_int]
@@ -246,6 +249,15 @@ class LobBatch:
         out = torch.empty((self.K, LOB_NSTATS), dtype=torch.int64, device=self.device)
         with torch.cuda.device(self.device):
             _check(lib().lob_get_stats(self.ctx, _ptr(out), _stream(stream)), "lob_get_stats")
+        return out
+
+
+    def digest(self, stream=None):
+        """[K] per-book FNV-1a-64 of the exported book, trade log, n_trades and counters
+        (lob_digest), as int64 bit patterns (torch has no uint64 arithmetic)."""
+        out = torch.empty((self.K,), dtype=torch.int64, device=self.device)
+        with torch.cuda.device(self.device):
+            _check(lib().lob_digest(self.ctx, _ptr(out), _stream(stream)), "lob_digest")
         return out
 
 

@@ -140,6 +140,10 @@ def test_full_size_c4_sampled_books():
                       lobgen.INIT_TS, lobgen.INIT_TNS)
     got = {k: v[sample] for k, v in g.items()}
     assert_outputs_equal(got, want, what="C4 full-size sample")
+    from digest import state_digest
+    dg = e.b.digest().cpu().numpy().view(np.uint64)
+    np.testing.assert_array_equal(dg[sample], state_digest(want["book"], want["trades"], want["n_trades"],
+                                                           want["stats"]))
     # properties that hold at any size, on every book
     st = g["stats"]
     assert (st[:, STAT_NAMES.index("msgs")] == cfg.n_msgs).all()
@@ -147,6 +151,27 @@ def test_full_size_c4_sampled_books():
     l2 = g["l2"]
     both = (l2[..., 0] > 0) & (l2[..., 2] > 0)
     assert (l2[..., 0, 0][both[..., 0]] > l2[..., 0, 2][both[..., 0]]).all()  # never crossed
+
+
+# ------------------------------------------- lob_digest (SURVEY.md 8(e) full-state fingerprint)
+@pytest.mark.parametrize("name,n,profile,Tcap", [("C2", 60, None, None), ("C5_2048", 6, None, None),
+                                                 ("C5_32", 300, "overflow", 3), ("C1", 1, "garbage", 0)])
+def test_digest_matches_oracle_state(name, n, profile, Tcap):
+    from digest import state_digest
+    cfg = lobgen.CONFIGS[name].with_(n_books=n)
+    if profile:
+        cfg = cfg.with_(profile=profile)
+    if Tcap is not None:
+        cfg = cfg.with_(trades_cap=Tcap)
+    msgs, init = lobgen.generate(cfg)
+    e = GpuEngine(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
+    run_engine(e, cfg, msgs, init, lobgen.INIT_TS, lobgen.INIT_TNS)
+    got = e.b.digest().cpu().numpy().view(np.uint64)
+    o = oracle.OracleBatch(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels, threads=8)
+    w = run_engine(o, cfg, msgs, init, lobgen.INIT_TS, lobgen.INIT_TNS)
+    want = state_digest(w["book"], w["trades"], w["n_trades"], w["stats"])
+    np.testing.assert_array_equal(got, want)
+    assert len(np.unique(got)) == cfg.n_books or cfg.n_books == 1   # books differ, so must digests
 
 
 # ------------------------------------------- NEXT row N1: per-message Level-1 trace
