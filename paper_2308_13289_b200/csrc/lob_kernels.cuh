@@ -239,42 +239,44 @@ struct Engine {
     __device__ __forceinline__ uint32_t bt_addr(int sd, int k) const { return sc + 8u * NST + 4u * (2 * sd + k); }
 
     // ---- group reductions: warp REDUX, then (W > 1) one exchange through shared memory
-    template <class Op>
-    __device__ __forceinline__ unsigned exchange(unsigned r, Op op) {
-        const uint32_t base = sc + 8u * NST + 16u + 4u * (uint32_t)(xph * W);
-        if ((tid & 31) == 0) sts32(base + 4u * (tid >> 5), (int)r);
+    // (two phases of 16 B per warp, alternated so one barrier per exchange suffices)
+    __device__ __forceinline__ uint32_t xbase() const { return sc + 8u * NST + 16u + 16u * (uint32_t)(xph * W); }
+    // after the barrier lane k < W holds warp k's partial and the other lanes `ident`,
+    // so a second warp REDUX finishes the group reduction
+    __device__ __forceinline__ unsigned exchange(unsigned r, unsigned ident) {
+        const uint32_t base = xbase();
+        if ((tid & 31) == 0) sts32(base + 16u * (tid >> 5), (int)r);
         __syncthreads();
-        unsigned m = (unsigned)lds32(base);
-#pragma unroll
-        for (int k = 1; k < W; ++k) m = op(m, (unsigned)lds32(base + 4u * k));
+        const int lane = tid & 31;
+        const unsigned v = lane < W ? (unsigned)lds32(base + 16u * lane) : ident;
         xph ^= 1;  // the other buffer next time: no write-after-read race with one barrier
-        return m;
+        return v;
     }
     __device__ __forceinline__ unsigned gmin_u(unsigned x) {
         const unsigned r = __reduce_min_sync(FULL, x);
         if constexpr (W == 1) return r;
-        else return exchange(r, [](unsigned a, unsigned b) { return a < b ? a : b; });
+        else return __reduce_min_sync(FULL, exchange(r, 0xffffffffu));
     }
     __device__ __forceinline__ int gmin_i(int x) {
         const int r = __reduce_min_sync(FULL, x);
         if constexpr (W == 1) return r;
-        else return (int)exchange((unsigned)r, [](unsigned a, unsigned b) { return (int)a < (int)b ? a : b; });
+        else return __reduce_min_sync(FULL, (int)exchange((unsigned)r, (unsigned)INT_MAX));
     }
     __device__ __forceinline__ unsigned gadd(unsigned x) {
         const unsigned r = __reduce_add_sync(FULL, x);
         if constexpr (W == 1) return r;
-        else return exchange(r, [](unsigned a, unsigned b) { return a + b; });
+        else return __reduce_add_sync(FULL, exchange(r, 0u));
     }
     __device__ __forceinline__ bool gany(bool b) {
         if constexpr (W == 1) return __any_sync(FULL, b);
-        else return exchange(__any_sync(FULL, b) ? 1u : 0u, [](unsigned a, unsigned c) { return a | c; }) != 0u;
+        else return __any_sync(FULL, exchange(__any_sync(FULL, b) ? 1u : 0u, 0u) != 0u);
     }
     // value held by thread `owner` of the group, to every thread
     __device__ __forceinline__ int bcast(int x, int owner) {
         if constexpr (W == 1) {
             return __shfl_sync(FULL, x, owner);
         } else {
-            const uint32_t base = sc + 8u * NST + 16u + 4u * (uint32_t)(xph * W);
+            const uint32_t base = xbase();
             if (tid == owner) sts32(base, x);
             __syncthreads();
             const int r = lds32(base);
@@ -298,6 +300,10 @@ struct Engine {
     // Eq.5 + G1), then earliest (Ts, Tns), then lowest slot (G4).
     template <int SD>
     __device__ __forceinline__ void recompute_best() {
+        if constexpr (W > 1) {
+            recompute_best_multi<SD>();
+            return;
+        }
         int lk = INT_MAX;
         bool has = false;
 #pragma unroll
@@ -339,6 +345,55 @@ struct Engine {
         const int2 bt = bk.times(SD, slot);  // broadcast shared load
         set_bt<SD>(bt.x, bt.y);
     }
+    // W > 1: the same key order with two barriers instead of four to six.  Resting
+    // prices are >= 1 (G22), so the offset key below is < 0xffffffff for every
+    // occupied slot and the all-ones value doubles as "side empty".  The time
+    // tie-break runs as a warp-level lexicographic (Ts, Tns, slot) minimum whose W
+    // winners are exchanged once.
+    template <int SD>
+    __device__ __forceinline__ void recompute_best_multi() {
+        unsigned lk = 0xffffffffu;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+            if (q > 0) lk = min(lk, k);
+        }
+        const unsigned m = gmin_u(lk);
+        if (m == 0xffffffffu) { bslot[SD] = BEST_EMPTY; return; }
+        int lts = INT_MAX, ltns = INT_MAX, lj = -1;
+        unsigned lv = 0;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+            if (q > 0 && k == m) {
+                const int2 t2 = bk.times(SD, j * GT + tid);
+                if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
+                lv += (unsigned)q;
+            }
+        }
+        if constexpr (TL1) bV[SD] = gadd(lv);
+        const bool in = lj >= 0;
+        const int w1 = __reduce_min_sync(FULL, in ? lts : INT_MAX);
+        const bool in1 = in && lts == w1;
+        const int w2 = __reduce_min_sync(FULL, in1 ? ltns : INT_MAX);
+        const unsigned w3 = __reduce_min_sync(FULL, (in1 && ltns == w2) ? (unsigned)(lj * GT + tid) : 0xffffffffu);
+        const uint32_t base = xbase();
+        if ((tid & 31) == 0) sts128(base + 16u * (tid >> 5), make_int4(w1, w2, (int)w3, 0));
+        __syncthreads();
+        const int lane = tid & 31;  // lane k < W takes warp k's winner; the same REDUXes again
+        const int4 c = lane < W ? lds128(base + 16u * lane) : make_int4(INT_MAX, INT_MAX, -1, 0);
+        xph ^= 1;
+        const int b1 = __reduce_min_sync(FULL, c.x);
+        const bool c1 = c.x == b1;
+        const int b2 = __reduce_min_sync(FULL, c1 ? c.y : INT_MAX);
+        const unsigned b3 = __reduce_min_sync(FULL, (c1 && c.y == b2) ? (unsigned)c.z : 0xffffffffu);
+        bslot[SD] = (int)b3;
+        bP[SD] = (SD == ASK) ? (int)(m + 1u) : (int)(INT_MAX - (int)m);
+        set_bt<SD>(b1, b2);
+    }
+
     template <int SD>
     __device__ __forceinline__ void set_bt(int ts, int tns) {
         if constexpr (kBtRegs) {
@@ -457,8 +512,12 @@ struct Engine {
                 bk.v[OWN][F_OID][J] = mOID;
             }
         });
-        if (tid == 0) bk.put_cold(OWN, slot, mTID, mTS, mTNS);  // one writer, published below
-        group_sync<W>();
+        if (tid == 0) bk.put_cold(OWN, slot, mTID, mTS, mTNS);  // one writer
+        // W = 1: __syncwarp publishes it to the lanes' next cold reads.  W > 1: cold
+        // records are read only inside recompute_best_multi, after its first barrier,
+        // and every such read completes before its second barrier, so the barriers
+        // already order this write against earlier and later reads.
+        if constexpr (W == 1) group_sync<W>();
         note_add<OWN>(slot, mP, mTS, mTNS, Qa);
     }
 
@@ -537,7 +596,7 @@ struct Engine {
 // Per-book shared scratch: counters [NST] int64, best times [2][2] int32,
 // cross-warp exchange buffers [2][W] u32.
 template <int W>
-constexpr int scratch_bytes() { return 8 * NST + 16 + 8 * W + 8; }
+constexpr int scratch_bytes() { return 8 * NST + 16 + (W == 1 ? 8 : 32 * W) + 8; }
 
 // Dynamic shared memory of one CTA of G books of (KPL, W).
 template <int KPL, int W, int G>
@@ -574,8 +633,9 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
     uint32_t chunk_seq = 0;
     // dynamic book scheduling: deep sweeps make books unequal, so after its first
     // (static) book a group takes the next one from a global counter when it is free
-    const uint32_t next_addr = scratch + 8u * NST + 16u + 8u * W;
+    const uint32_t next_addr = scratch + 8u * NST + 16u + (W == 1 ? 8u : 32u * W);
     const int groups = gridDim.x * G;
+    const bool multi = groups < p.nb;  // more books than groups: dynamic scheduling (sched counters)
     int lb = blockIdx.x * G + g;
     while (lb < p.nb) {
         const int b = p.book0 + lb;
@@ -665,6 +725,7 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
             p.stats[(size_t)b * NST + tid] += v;
         }
         if (tid == 0) p.ntrades[b] = logged;
+        if (!multi) break;  // one wave: every book had a group of its own
         int next = 0;
         if (tid == 0) next = groups + (int)atomicAdd(p.sched, 1u);
         if constexpr (W == 1) {
@@ -676,7 +737,7 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
         }
     }
     // the last group to finish re-arms the counters for the next launch
-    if (tid == 0) {
+    if (multi && tid == 0) {
         __threadfence();
         if (atomicAdd(p.sched + 1, 1u) == gridDim.x * G - 1) {
             atomicExch(p.sched, 0u);

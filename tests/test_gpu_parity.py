@@ -62,6 +62,16 @@ def test_profiles(profile, N):
     assert_outputs_equal(g, o, what=f"{profile} N={N}")
 
 
+@pytest.mark.parametrize("N", [31, 32, 33, 64, 65, 96, 128, 129, 256, 257, 512, 513, 1024, 1025, 2047, 2048])
+def test_geometry_boundaries(N):
+    # every (rows per thread, warps per book) geometry and both sides of each boundary
+    # (lob_api.cu geo_of: KPL = 1/2/3/4/8 with one warp, then 2/4/8 warps of 8 rows)
+    for profile in ("ties", "overflow"):
+        cfg = lobgen.Config("geo", 45, N, 4, 60, min(N, 10), 40, 10, profile, 7 * N + len(profile))
+        g, o = _both(cfg)
+        assert_outputs_equal(g, o, what=f"{profile} N={N}")
+
+
 @pytest.mark.parametrize("L,Tcap", [(1, 0), (32, 3), (10, 1)])
 def test_levels_and_tiny_trade_log(L, Tcap):
     cfg = lobgen.Config("p", 200, 100, 5, 50, 40, Tcap, L, "heavy_market", 5)
