@@ -86,6 +86,9 @@ CONFIGS = {
     "C5_100": Config("C5_100", 4096, 100, 10, 100, 33, 1024, 10, "lobster", 5),
     "C5_512": Config("C5_512", 4096, 512, 10, 100, 170, 1024, 10, "lobster", 5),
     "C5_2048": Config("C5_2048", 4096, 2048, 10, 100, 682, 1024, 10, "lobster", 5),
+    # extra points of the same sweep (not BASELINE configs): the other kernel geometries
+    "C5_256": Config("C5_256", 4096, 256, 10, 100, 85, 1024, 10, "lobster", 5),
+    "C5_1024": Config("C5_1024", 4096, 1024, 10, 100, 341, 1024, 10, "lobster", 5),
 }
 
 
