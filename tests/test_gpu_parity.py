@@ -114,6 +114,44 @@ def test_determinism_clones_and_isolation():
     assert (st == st[:1]).all()
 
 
+@pytest.mark.parametrize("K", [300, 6000])
+def test_cuda_graph_mode_a(K):
+    # C2's RL shape, one call per step, captured once in a CUDA graph and replayed:
+    # one wave of books (K = 300) and dynamic scheduling across waves (K = 6000)
+    from paper_2308_13289_b200 import LobBatch
+    cfg = lobgen.CONFIGS["C2"].with_(n_books=K, n_steps=6)
+    msgs, init = lobgen.generate(cfg)
+    M, L = cfg.msgs_per_step, cfg.l2_levels
+    b = LobBatch(K, cfg.capacity, cfg.trades_cap, L)
+    steps = [torch.from_numpy(np.ascontiguousarray(msgs[:, s * M:(s + 1) * M])).cuda() for s in range(cfg.n_steps)]
+    ti = torch.from_numpy(init).cuda()
+    l2 = torch.empty((cfg.n_steps, K, 1, L, 4), dtype=torch.int32, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # warm-up outside capture
+        b.init(ti, lobgen.INIT_TS, lobgen.INIT_TNS)
+        b.process(steps[0], 1, M, l2_out=l2[0])
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        b.init(ti, lobgen.INIT_TS, lobgen.INIT_TNS)
+        for s in range(cfg.n_steps):
+            b.process(steps[s], 1, M, l2_out=l2[s])
+    for _ in range(2):  # replays are independent episodes from the same initial state
+        l2.fill_(7)
+        g.replay()
+        torch.cuda.synchronize()
+    o = oracle.OracleBatch(K, cfg.capacity, cfg.trades_cap, L, threads=8)
+    want = run_engine(o, cfg, msgs, init, lobgen.INIT_TS, lobgen.INIT_TNS, calls=cfg.n_steps)
+    np.testing.assert_array_equal(l2[:, :, 0].permute(1, 0, 2, 3).cpu().numpy(), want["l2"])
+    np.testing.assert_array_equal(b.book().cpu().numpy(), want["book"])
+    np.testing.assert_array_equal(b.stats().cpu().numpy(), want["stats"])
+    tr, cnt = b.trades()
+    np.testing.assert_array_equal(cnt.cpu().numpy(), want["n_trades"])
+    np.testing.assert_array_equal(tr.cpu().numpy(), want["trades"])
+
+
 def test_host_path_equals_device_path():
     cfg = lobgen.CONFIGS["C4"].with_(n_books=3000)
     msgs, init = lobgen.generate(cfg)
@@ -349,3 +387,60 @@ def test_env_rollout_parity(K, N, side, episode):
         assert np.all(np.abs(rg - ro) <= 1e-12 * np.maximum(1.0, scale)), (s, np.abs(rg - ro).max())
         np.testing.assert_array_equal(ge.book(), oe.book())
         np.testing.assert_array_equal(ge.stats(), oe.stats())
+
+
+def test_env_episode_in_cuda_graph():
+    """A whole N3 episode (book init, env reset, 10 env steps) captured once in a CUDA
+    graph and replayed twice: per-step rewards, done flags, executed quantities and the
+    final books equal the oracle's eager rollout (rewards within 1e-12 of their terms)."""
+    from paper_2308_13289_b200 import LobBatch
+    K, N, S = 800, 100, 10
+    cfg = lobgen.Config("env", K, N, S, 100, 33, 512, 10, "lobster", 91)
+    msgs, init = lobgen.generate(cfg)
+    kw = dict(task_side=1, task_size=2500, n_passive=2, tick=100, episode_s=900, agent_tid=77,
+              agent_oid_base=2_000_000_000, reserved=0, lam=0.5)
+    _, oe, gcfg, ocfg, LobEnv = _env_pair(K, N, kw, init)
+    b = LobBatch(K, N, 512, 10)
+    env = LobEnv(b, gcfg, 100)
+    rng = np.random.default_rng(5)
+    acts = [torch.from_numpy(rng.uniform(-50, 400, (K, 4)).astype(np.float32)).cuda() for _ in range(S)]
+    data = [torch.from_numpy(np.ascontiguousarray(msgs[:, s * 100:(s + 1) * 100])).cuda() for s in range(S)]
+    ti = torch.from_numpy(init).cuda()
+    rew = torch.empty((S, K), dtype=torch.float64, device="cuda")
+    dn = torch.empty((S, K), dtype=torch.int32, device="cuda")
+    ex = torch.empty((S, K), dtype=torch.int64, device="cuda")
+
+    def episode():
+        b.init(ti, lobgen.INIT_TS, lobgen.INIT_TNS)
+        env.reset(lobgen.INIT_TS, lobgen.INIT_TNS)
+        for s in range(S):
+            r, d, x = env.step(acts[s], data[s])
+            rew[s].copy_(r)
+            dn[s].copy_(d)
+            ex[s].copy_(x)
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        episode()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        episode()
+    for _ in range(2):
+        rew.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+    oenv = oracle.OracleEnv(oe, ocfg)
+    oenv.reset(lobgen.INIT_TS, lobgen.INIT_TNS)
+    prev = np.zeros(K, np.int64)
+    for s in range(S):
+        ro, do, xo, _ = oenv.step(acts[s].cpu().numpy(), np.ascontiguousarray(msgs[:, s * 100:(s + 1) * 100]), 100)
+        np.testing.assert_array_equal(dn[s].cpu().numpy(), do)
+        np.testing.assert_array_equal(ex[s].cpu().numpy(), xo)
+        scale = (xo - prev).astype(np.float64) * 4e6 * (1 + kw["lam"])
+        prev = xo.copy()
+        assert np.all(np.abs(rew[s].cpu().numpy() - ro) <= 1e-12 * np.maximum(1.0, scale)), s
+    np.testing.assert_array_equal(b.book().cpu().numpy(), oe.book())
+    np.testing.assert_array_equal(b.stats().cpu().numpy(), oe.stats())
