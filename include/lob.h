@@ -166,14 +166,16 @@ size_t lob_env_state_bytes(int32_t n_envs);
 int lob_env_reset(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, int32_t init_ts,
                   int32_t init_tns, void *cuda_stream);
 
-/* One env step in every book (3 kernel launches on cuda_stream):
+/* One env step in every book, ONE kernel launch on cuda_stream (the agent's messages,
+ * then the step's data, then reward / time / termination, fused per book):
  *  d_actions [K][4] f32: sizes at the far-touch, mid, near-touch and passive prices
  *  (P:L476-493), rounded half-even, negative/NaN -> 0, capped far-touch first by the
  *  remaining task; d_data [K][msgs_per_step][8]: the step's data messages (zero rows
- *  are padding, G21); d_work [K][8+msgs_per_step][8] int32 workspace that receives the
- *  step's stream (rows 0..7 the agent's messages, zero-padded); outputs (nullable):
+ *  are padding, G21); d_work [K][8][8] int32 receives the agent's messages of the step
+ *  (zero-padded; processed before the data); outputs (nullable):
  *  d_reward [K] f64 (eq:rewardfunc), d_done [K] int32, d_executed [K] int64, and the
- *  post-step L2 d_l2_out [K][1][L][4].  A finished env receives padding only. */
+ *  post-step L2 d_l2_out [K][1][L][4].  A finished env receives padding only (its
+ *  counters still count 8 + msgs_per_step messages). */
 int lob_env_step(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const float *d_actions,
                  const int32_t *d_data, int32_t msgs_per_step, int32_t *d_work, double *d_reward,
                  int32_t *d_done, int64_t *d_executed, int32_t *d_l2_out, void *cuda_stream);

@@ -75,7 +75,7 @@ struct lob_ctx {
     char *state;
     int sm_count;
     Geo geo;
-    int grid_cap;  // persistent grid: resident CTAs for the step kernel
+    int grid_cap[3];  // persistent grid: resident CTAs of the step kernel, per MODE
     int32_t *book() const { return reinterpret_cast<int32_t *>(state + lay.off_book); }
     int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
     int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
@@ -122,9 +122,10 @@ int after_launch(const char *what) {
 unsigned blocks_for(long long threads, int bs) { return (unsigned)((threads + bs - 1) / bs); }
 
 int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M, int32_t *d_l2, int book0, int nb,
-                cudaStream_t st, int32_t *d_l1 = nullptr) {
+                cudaStream_t st, int32_t *d_l1 = nullptr, const EnvParams *env = nullptr) {
     if (nb <= 0) return LOB_OK;
     Params p;
+    const EnvParams ep = env ? *env : EnvParams{};
     p.book = ctx->book(); p.trades = ctx->trades(); p.ntrades = ctx->ntr(); p.stats = ctx->stats();
     p.msgs = d_msgs; p.l2out = d_l2; p.l1out = d_l1; p.sched = ctx->sched();
     p.N = ctx->cfg.capacity; p.NP = ctx->lay.NP; p.Tcap = ctx->cfg.trades_cap; p.L = ctx->cfg.l2_levels;
@@ -133,9 +134,11 @@ int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M,
     for_geo(ctx->geo, [&](auto kc, auto wc, auto gc) {
         constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, G = decltype(gc)::value;
         const unsigned need = blocks_for(nb, G);
-        const unsigned grid = need < (unsigned)ctx->grid_cap ? need : (unsigned)ctx->grid_cap;
-        if (d_l1) lob_step<KPL, W, G, true><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p);
-        else lob_step<KPL, W, G, false><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p);
+        const unsigned cap = (unsigned)ctx->grid_cap[env ? 2 : (d_l1 ? 1 : 0)];
+        const unsigned grid = need < cap ? need : cap;
+        if (env) lob_step<KPL, W, G, 2><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p, ep);
+        else if (d_l1) lob_step<KPL, W, G, 1><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p, ep);
+        else lob_step<KPL, W, G, 0><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p, ep);
         rc = after_launch("lob_step kernel");
     });
     return rc;
@@ -171,23 +174,29 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
     c->state = static_cast<char *>(d_state);
     c->sm_count = sms;
     c->geo = geo_of(cfg->capacity);
-    int per_sm = 1;
+    int per_sm[3] = {1, 1, 1};
     int rc = LOB_OK;
     for_geo(c->geo, [&](auto kc, auto wc, auto gc) {
         constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, G = decltype(gc)::value;
         constexpr int smem = step_smem_bytes<KPL, W, G>();
-        e = cudaFuncSetAttribute(lob_step<KPL, W, G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        e = cudaFuncSetAttribute(lob_step<KPL, W, G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lob_step<KPL, W, G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            e = cudaFuncSetAttribute(lob_step<KPL, W, G, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lob_step<KPL, W, G, false>, 32 * W * G, smem);
+            e = cudaFuncSetAttribute(lob_step<KPL, W, G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], lob_step<KPL, W, G, 0>, 32 * W * G, smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], lob_step<KPL, W, G, 1>, 32 * W * G, smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[2], lob_step<KPL, W, G, 2>, 32 * W * G, smem);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(lob_export_l2<KPL, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      export_l2_smem_bytes<KPL, W>());
         if (e != cudaSuccess) rc = cuda_fail(e, "kernel attribute / occupancy query");
     });
     if (rc != LOB_OK) { delete c; return rc; }
-    c->grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    for (int m = 0; m < 3; ++m) c->grid_cap[m] = sms * (per_sm[m] > 0 ? per_sm[m] : 1);
     *out = c;
     return LOB_OK;
 }
@@ -365,20 +374,16 @@ int lob_env_step(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const flo
         reinterpret_cast<uintptr_t>(d_data) % 16 || reinterpret_cast<uintptr_t>(d_l2_out) % 16 ||
         reinterpret_cast<uintptr_t>(d_reward) % 8 || reinterpret_cast<uintptr_t>(d_executed) % 8)
         return fail(LOB_EINVAL, "misaligned buffer%s");
-    EnvCfg c;
-    memcpy(&c, cfg, sizeof c);
-    cudaStream_t st = (cudaStream_t)stream;
-    EnvState *env = static_cast<EnvState *>(d_env);
-    lob_env_actions_kernel<<<blocks_for(K, 8), 256, 0, st>>>(ctx->book(), ctx->cfg.capacity, ctx->lay.NP, K, env, c,
-                                                             d_actions, d_data, msgs_per_step, d_work);
-    rc = after_launch("lob_env_actions_kernel");
-    if (rc) return rc;
-    rc = launch_step(ctx, d_work, 1, 8 + msgs_per_step, d_l2_out, 0, K, st);
-    if (rc) return rc;
-    lob_env_post_kernel<<<blocks_for(K, 8), 256, 0, st>>>(ctx->trades(), ctx->ntr(), ctx->cfg.trades_cap, K, env, c,
-                                                          d_data, msgs_per_step, d_reward, d_done,
-                                                          reinterpret_cast<long long *>(d_executed));
-    return after_launch("lob_env_post_kernel");
+    EnvParams ep{};
+    memcpy(&ep.ec, cfg, sizeof ep.ec);
+    ep.env = static_cast<EnvState *>(d_env);
+    ep.actions = d_actions;
+    ep.agent_out = d_work;
+    ep.reward = d_reward;
+    ep.done = d_done;
+    ep.executed = reinterpret_cast<long long *>(d_executed);
+    // one fused launch: agent messages, the step's data, reward / time / termination
+    return launch_step(ctx, d_data, 1, msgs_per_step, d_l2_out, 0, K, (cudaStream_t)stream, nullptr, &ep);
 }
 
 int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *stream) {

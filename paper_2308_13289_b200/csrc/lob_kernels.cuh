@@ -47,6 +47,24 @@ constexpr int BEST_INVALID = -2, BEST_EMPTY = -1;
 template <int I>
 using IC = std::integral_constant<int, I>;
 
+// NEXT row N3 (execution env, Sec.5.1.3 / 5.2): the task shared by all envs
+// and the per-env state (see lob_env.cuh, include/lob.h lob_env_config)
+struct EnvCfg {  // == lob_env_config (include/lob.h)
+    int task_side, task_size, n_passive, tick, episode_s, agent_tid, oid_base, reserved;
+    double lam;
+};
+struct EnvState {  // 64 bytes per env
+    long long executed;
+    double p_init;
+    int init_ts, init_tns, cur_ts, cur_tns, next_oid, done, last_ask, last_bid;
+    int live[4];
+};
+static_assert(sizeof(EnvState) == 64, "env state layout");
+
+__device__ __forceinline__ long long env_elapsed_ns(const EnvState &e) {
+    return ((long long)e.cur_ts - e.init_ts) * 1000000000LL + ((long long)e.cur_tns - e.init_tns);
+}
+
 struct Params {
     int32_t *book;         // [K][2][NF][NP] SoA, slot i at [i] (i = row*GT + tid)
     int32_t *trades;       // [K][Tcap][6]
@@ -58,6 +76,17 @@ struct Params {
     unsigned *sched;       // [2]: next book, finished groups (zero between launches)
     int N, NP, Tcap, L, n_steps, M;
     int book0, nb;         // books [book0, book0+nb) of the state
+};
+// MODE 2 only (fused env step, NEXT N3; Params::msgs = the step's data messages).  A
+// separate kernel parameter, so the other modes' parameter block is unchanged.
+struct EnvParams {
+    EnvState *env;         // [K]
+    const float *actions;  // [K][4]
+    int32_t *agent_out;    // [K][8][8]: the agent's messages of the step, zero-padded
+    double *reward;        // [K] or null
+    int32_t *done;         // [K] or null
+    long long *executed;   // [K] or null
+    EnvCfg ec;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -598,6 +627,141 @@ struct Engine {
 template <int W>
 constexpr int scratch_bytes() { return 8 * NST + 16 + (W == 1 ? 8 : 32 * W) + 8; }
 
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    return x;
+}
+
+// ---------------------------------------------------- NEXT N3: fused env step
+// The agent's action -> at most 8 messages, processed before the step's data
+// (P:L417-418): cancel (delete) the previous step's orders (E1); then either the
+// forced market order one minute before the end or one limit order per
+// positive size at the far-touch / mid / near-touch / passive prices (P:L476-493,
+// P:L457-465; E2-E6).  Every price comes from the book as it was before the
+// first agent message.  All values are group-uniform; the messages are also
+// written to agent_out (thread 0) for observability.
+template <class E>
+__device__ __forceinline__ void env_agent(E &e, EnvState &es, const Params &p, const EnvParams &ep, int b, int tid) {
+    const EnvCfg &c = ep.ec;
+    int4 *out = reinterpret_cast<int4 *>(ep.agent_out + (size_t)b * 64);
+    int n = 0;
+    if (!es.done) {
+        if (e.bslot[ASK] == BEST_INVALID) e.template recompute_best<ASK>();
+        if (e.bslot[BID] == BEST_INVALID) e.template recompute_best<BID>();
+        int ask = e.bslot[ASK] >= 0 ? e.bP[ASK] : -1, bid = e.bslot[BID] >= 0 ? e.bP[BID] : -1;
+        const int S = c.task_side;
+        long long remaining = (long long)c.task_size - es.executed;
+        const bool forced = remaining > 0 && env_elapsed_ns(es) >= ((long long)c.episode_s - 60) * 1000000000LL;
+        const bool limits = remaining > 0 && !forced;
+        int pr0 = 0, pr1 = 0, pr2 = 0, pr3 = 0;
+        if (limits) {
+            if (ask > 0) es.last_ask = ask; else ask = es.last_ask;  // E6
+            if (bid > 0) es.last_bid = bid; else bid = es.last_bid;
+            const int far = (S == -1) ? bid : ask, near = (S == -1) ? ask : bid;
+            pr0 = far;
+            pr2 = near;
+            pr3 = near > 0 ? near - S * c.n_passive * c.tick : 0;
+            if (ask > 0 && bid > 0) {  // E5: the tick at or beyond the mid, away from the spread
+                const long long twice = (long long)ask + bid, t2 = 2LL * c.tick;
+                const long long q = twice / t2, rmd = twice % t2;
+                pr1 = (int)((S == -1 && rmd) ? (q + 1) * c.tick : q * c.tick);
+            }
+        }
+        const int l0 = es.live[0], l1 = es.live[1], l2 = es.live[2], l3 = es.live[3];
+        int n0 = 0, n1 = 0, n2 = 0, n3 = 0, li = 0;
+        for (int k = 0; k < 9; ++k) {
+            int T = 0, Q = 0, P = 0, O = 0;
+            if (k < 4) {  // E1
+                const int l = k == 0 ? l0 : (k == 1 ? l1 : (k == 2 ? l2 : l3));
+                if (l != 0) { T = 3; Q = INT_MAX; O = l; }
+            } else if (k == 4) {
+                if (forced) { T = 4; Q = (int)(remaining > INT_MAX ? INT_MAX : remaining); O = es.next_oid++; }
+            } else if (limits) {
+                const int j = k - 5;
+                const float x = ep.actions[4 * (size_t)b + j];
+                long long q = 0;  // E2: round half-even, NaN / negative -> 0
+                if (x == x && x > 0.0f) q = (x >= 2147483647.0f) ? 2147483647LL : (long long)__float2int_rn(x);
+                if (q > remaining) q = remaining;  // E3
+                const int pr = j == 0 ? pr0 : (j == 1 ? pr1 : (j == 2 ? pr2 : pr3));
+                if (q > 0 && pr > 0) {
+                    remaining -= q;
+                    T = 1; Q = (int)q; P = pr; O = es.next_oid++;
+                    n0 = li == 0 ? O : n0; n1 = li == 1 ? O : n1; n2 = li == 2 ? O : n2; n3 = li == 3 ? O : n3;
+                    ++li;
+                }
+            }
+            if (T != 0) {
+                const int4 a = make_int4(T, S, Q, P), bb = make_int4(O, c.agent_tid, es.cur_ts, es.cur_tns);
+                if (tid == 0) { out[2 * n] = a; out[2 * n + 1] = bb; }
+                ++n;
+                e.message(a, bb);
+            }
+        }
+        es.live[0] = n0; es.live[1] = n1; es.live[2] = n2; es.live[3] = n3;
+    }
+    if (tid == 0)
+        for (int i = n; i < 8; ++i) out[2 * i] = out[2 * i + 1] = make_int4(0, 0, 0, 0);
+}
+
+// After the step: reward over the step's logged trades (eq:rewardfunc / eq:vwap,
+// P:L498-506, agent = OIDs [oid_base, next_oid), G29; the same sums as
+// lob_reward_kernel), executed quantity, time := the last data message,
+// termination.  The group's first warp; trades were written
+// by their owner threads, hence the barrier.
+template <int W>
+__device__ __forceinline__ void env_post(const Params &p, const EnvParams &ep, int b, int tid, int n, bool have_last,
+                                         int last_ts, int last_tns) {
+    const EnvCfg &c = ep.ec;
+    group_sync<W>();  // also publishes env_agent's state write (thread 0)
+    if (tid >= 32) return;
+    EnvState es = ep.env[b];
+    const int lane = tid;
+    if (es.done) {  // finished before this step (E8)
+        if (lane == 0) {
+            if (ep.reward) ep.reward[b] = 0.0;
+            if (ep.done) ep.done[b] = 1;
+            if (ep.executed) ep.executed[b] = es.executed;
+        }
+        return;
+    }
+    const int2 *t = reinterpret_cast<const int2 *>(p.trades + (size_t)b * p.Tcap * 6);
+    double sqp = 0.0, sq = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const int2 pq = t[3 * i];
+        sqp += (double)pq.y * (double)pq.x;
+        sq += (double)pq.y;
+    }
+    sqp = warp_sum(sqp);
+    sq = warp_sum(sq);
+    const double v = sq > 0.0 ? sqp / sq : 0.0;
+    const int lo = c.oid_base, hi = es.next_oid - 1;
+    double adv = 0.0, drift = 0.0;
+    long long qa = 0;
+    for (int i = lane; i < n && sq > 0.0; i += 32) {
+        const int2 pq = t[3 * i], oo = t[3 * i + 1];
+        if ((oo.x >= lo && oo.x <= hi) || (oo.y >= lo && oo.y <= hi)) {
+            adv += (double)pq.y * ((double)pq.x - v);
+            drift += (double)pq.y * (v - es.p_init);
+            qa += pq.y;
+        }
+    }
+    adv = warp_sum(adv);
+    drift = warp_sum(drift);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qa += __shfl_xor_sync(FULL, qa, o);
+    if (lane == 0) {
+        es.executed += qa;
+        if (have_last) { es.cur_ts = last_ts; es.cur_tns = last_tns; }
+        es.done = (es.executed >= c.task_size) || (env_elapsed_ns(es) > (long long)c.episode_s * 1000000000LL);
+        const double r = adv + c.lam * drift;
+        if (ep.reward) ep.reward[b] = c.task_side == 1 ? -r : r;
+        if (ep.done) ep.done[b] = es.done;
+        if (ep.executed) ep.executed[b] = es.executed;
+        ep.env[b] = es;
+    }
+}
+
 // Dynamic shared memory of one CTA of G books of (KPL, W).
 template <int KPL, int W, int G>
 constexpr int step_smem_bytes() {
@@ -608,11 +772,13 @@ constexpr int step_smem_bytes() {
 #define MINB4 7
 #endif
 // Persistent: group g of CTA b starts with book b*G + g, then takes books from the
-// dynamic counter.  TL1 also writes the Level-1 trace (NEXT N1).
-template <int KPL, int W, int G, bool TL1>
+// dynamic counter.  MODE 0: L2 per step; MODE 1 also writes the Level-1 trace (NEXT
+// N1); MODE 2 is one fused execution-env step (NEXT N3, env_agent / env_post).
+template <int KPL, int W, int G, int MODE>
 __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : 16 / W))))
-    lob_step(const Params p) {
+    lob_step(const Params p, const EnvParams ep) {
     using BK = RegBook<KPL, W>;
+    constexpr bool TL1 = MODE == 1, ENV = MODE == 2;
     extern __shared__ __align__(128) unsigned char dyn[];
     const int g = threadIdx.x / (32 * W);
     const int tid = (int)opaque(threadIdx.x % (32 * W));
@@ -666,6 +832,15 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
         e.bV[0] = e.bV[1] = 0;
         int32_t *l1dst = TL1 ? p.l1out + (size_t)lb * nmsg * 4 : nullptr;
         int left = p.M, step = 0;
+        [[maybe_unused]] int last_ts = 0, last_tns = 0;
+        [[maybe_unused]] bool idle = false, have_last = false;
+        if constexpr (ENV) {  // the agent's messages go first
+            EnvState es = ep.env[b];
+            idle = es.done != 0;  // a finished env only sees padding (E8)
+            env_agent(e, es, p, ep, b, tid);
+            if (tid == 0) ep.env[b] = es;  // re-read by env_post: not live across the message loop
+            if (nmsg == 0 && p.l2out) e.l2_write(p.l2out + (size_t)lb * p.L * 4, p.L);
+        }
         for (int c = 0; c < nchunks; ++c) {
             const uint32_t seq = chunk_seq + c, slot = seq & 1;
             mbar_wait(bars + 8 * slot, (seq >> 1) & 1);
@@ -676,7 +851,14 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
                 const uint32_t mend = maddr + 32u * run;
                 do {
                     const int4 a = lds128(maddr), bb = lds128(maddr + 16);
-                    e.message(a, bb);
+                    if constexpr (ENV) {
+                        if (!idle) {
+                            e.message(a, bb);
+                            if (a.x != 0) { last_ts = bb.z; last_tns = bb.w; have_last = true; }
+                        }
+                    } else {
+                        e.message(a, bb);
+                    }
                     if constexpr (TL1) {
                         e.l1_write(l1dst);
                         l1dst += 4;
@@ -720,11 +902,12 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 
         if (tid < NST) {
             long long v = lds64(scratch + 8u * tid);
             if (tid == ST_DROPPED) v += e.ntr - logged;
-            if (tid == ST_MSGS) v += nmsg;
+            if (tid == ST_MSGS) v += nmsg + (ENV ? 8 : 0);  // env: 8 agent rows + data (E8)
             if (tid == ST_TRADES) v += e.ntr;  // fills = logged + dropped
             p.stats[(size_t)b * NST + tid] += v;
         }
         if (tid == 0) p.ntrades[b] = logged;
+        if constexpr (ENV) env_post<W>(p, ep, b, tid, logged, have_last, last_ts, last_tns);
         if (!multi) break;  // one wave: every book had a group of its own
         int next = 0;
         if (tid == 0) next = groups + (int)atomicAdd(p.sched, 1u);
@@ -791,11 +974,6 @@ __global__ void lob_init_kernel(int32_t *book, int32_t *trades, int32_t *ntrades
 // the summation order.  R = sum_j Q_j (P_j - P_VWAP) + lambda sum_j Q_j (P_VWAP -
 // P_init) over the agent's trades j (eq:rewardfunc; agent = aggressor or
 // standing OID in the book's range, G29); buy task negates (G30); no trades -> 0 (G31).
-__device__ __forceinline__ double warp_sum(double x) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
-    return x;
-}
 __global__ void lob_reward_kernel(const int32_t *trades, const int32_t *ntrades, int K, int Tcap,
                                   const int32_t *agent, const double *p_init, const int32_t *side, double lambda,
                                   double *reward, double *vwap, long long *agent_qty) {

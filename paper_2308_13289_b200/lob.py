@@ -270,7 +270,7 @@ class LobEnv:
         L = lib()
         n = L.lob_env_state_bytes(batch.K)
         self.state = torch.empty(max(int(n), 64), dtype=torch.uint8, device=batch.device)
-        self.work = torch.empty((batch.K, 8 + self.M, 8), dtype=torch.int32, device=batch.device)
+        self.work = torch.empty((batch.K, 8, 8), dtype=torch.int32, device=batch.device)  # agent messages
         self.reward = torch.empty((batch.K,), dtype=torch.float64, device=batch.device)
         self.done = torch.empty((batch.K,), dtype=torch.int32, device=batch.device)
         self.executed = torch.empty((batch.K,), dtype=torch.int64, device=batch.device)

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """NEXT row N3 measurement: execution-env steps on the device (the shape of PAPER.md
 Table 6): K envs (one book each, N = 100, 10-level initial book), 100
-data messages per step, random actions.  Times lob_env_step (3 launches) eagerly and
+data messages per step, random actions.  Times lob_env_step (one fused launch) eagerly and
 as a captured CUDA graph; prints one JSON line."""
 import json
 import os
