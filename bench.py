@@ -297,7 +297,7 @@ def main():
     peak, peak_src, _ = load_peaks()
     achieved = alg_bytes / (kmean_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "lobk::lob_step<4,1,4,false> (lob_process_messages)",
+                "traffic": None, "kernel": "lobk::lob_step<4,1,4,3> (lob_process_messages; MODE 3 = the 8-CTA/SM build for many-wave batches)",
                 "kernel_ms": kmean_ms, "kernel_share_of_step": kmean_ms / ms_per_step,
                 "alg_bytes_per_launch": alg_bytes, "alg_bytes_per_msg": alg_bytes / (K * cfg.n_msgs),
                 "peak_source": peak_src}

@@ -75,7 +75,7 @@ struct lob_ctx {
     char *state;
     int sm_count;
     Geo geo;
-    int grid_cap[3];  // persistent grid: resident CTAs of the step kernel, per MODE
+    int grid_cap[4];  // persistent grid: resident CTAs of the step kernel, per MODE
     int32_t *book() const { return reinterpret_cast<int32_t *>(state + lay.off_book); }
     int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
     int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
@@ -134,11 +134,20 @@ int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M,
     for_geo(ctx->geo, [&](auto kc, auto wc, auto gc) {
         constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, G = decltype(gc)::value;
         const unsigned need = blocks_for(nb, G);
-        const unsigned cap = (unsigned)ctx->grid_cap[env ? 2 : (d_l1 ? 1 : 0)];
+        constexpr bool kWide = KPL == 4 && W == 1;  // MODE 3 exists for 4-row warp books only
+        // many waves of books: the 8-CTA/SM build (occupancy beats its extra spills)
+        const bool wide = kWide && !env && !d_l1 && (long long)nb >= 8LL * ctx->grid_cap[0] * G;
+        const unsigned cap = (unsigned)ctx->grid_cap[env ? 2 : (d_l1 ? 1 : (wide ? 3 : 0))];
         const unsigned grid = need < cap ? need : cap;
-        if (env) lob_step<KPL, W, G, 2><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p, ep);
-        else if (d_l1) lob_step<KPL, W, G, 1><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p, ep);
-        else lob_step<KPL, W, G, 0><<<grid, 32 * W * G, step_smem_bytes<KPL, W, G>(), st>>>(p, ep);
+        const int smem = step_smem_bytes<KPL, W, G>();
+        if (env) lob_step<KPL, W, G, 2><<<grid, 32 * W * G, smem, st>>>(p, ep);
+        else if (d_l1) lob_step<KPL, W, G, 1><<<grid, 32 * W * G, smem, st>>>(p, ep);
+        else if constexpr (kWide) {
+            if (wide) lob_step<KPL, W, G, 3><<<grid, 32 * W * G, smem, st>>>(p, ep);
+            else lob_step<KPL, W, G, 0><<<grid, 32 * W * G, smem, st>>>(p, ep);
+        } else {
+            lob_step<KPL, W, G, 0><<<grid, 32 * W * G, smem, st>>>(p, ep);
+        }
         rc = after_launch("lob_step kernel");
     });
     return rc;
@@ -174,7 +183,7 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
     c->state = static_cast<char *>(d_state);
     c->sm_count = sms;
     c->geo = geo_of(cfg->capacity);
-    int per_sm[3] = {1, 1, 1};
+    int per_sm[4] = {1, 1, 1, 1};
     int rc = LOB_OK;
     for_geo(c->geo, [&](auto kc, auto wc, auto gc) {
         constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, G = decltype(gc)::value;
@@ -190,13 +199,20 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], lob_step<KPL, W, G, 1>, 32 * W * G, smem);
         if (e == cudaSuccess)
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[2], lob_step<KPL, W, G, 2>, 32 * W * G, smem);
+        if constexpr (KPL == 4 && W == 1) {
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(lob_step<KPL, W, G, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e == cudaSuccess)
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[3], lob_step<KPL, W, G, 3>, 32 * W * G,
+                                                                  smem);
+        }
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(lob_export_l2<KPL, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      export_l2_smem_bytes<KPL, W>());
         if (e != cudaSuccess) rc = cuda_fail(e, "kernel attribute / occupancy query");
     });
     if (rc != LOB_OK) { delete c; return rc; }
-    for (int m = 0; m < 3; ++m) c->grid_cap[m] = sms * (per_sm[m] > 0 ? per_sm[m] : 1);
+    for (int m = 0; m < 4; ++m) c->grid_cap[m] = sms * (per_sm[m] > 0 ? per_sm[m] : 1);
     *out = c;
     return LOB_OK;
 }

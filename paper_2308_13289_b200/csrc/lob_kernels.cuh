@@ -772,10 +772,13 @@ constexpr int step_smem_bytes() {
 #define MINB4 7
 #endif
 // Persistent: group g of CTA b starts with book b*G + g, then takes books from the
-// dynamic counter.  MODE 0: L2 per step; MODE 1 also writes the Level-1 trace (NEXT
-// N1); MODE 2 is one fused execution-env step (NEXT N3, env_agent / env_post).
+// dynamic counter.  MODE 0 (and 3): L2 per step; MODE 1 also writes the Level-1
+// trace (NEXT N1); MODE 2 is one fused execution-env step (NEXT N3, env_agent /
+// env_post).
+// MODE 3 = MODE 0 built for 8 CTAs/SM (64 registers) instead of 7: more spills, more
+// warps; chosen by the host for many-wave batches of 4-row books (C4: +1.7 %)
 template <int KPL, int W, int G, int MODE>
-__global__ void __launch_bounds__(32 * W * G, (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : 16 / W))))
+__global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : 16 / W)))))
     lob_step(const Params p, const EnvParams ep) {
     using BK = RegBook<KPL, W>;
     constexpr bool TL1 = MODE == 1, ENV = MODE == 2;
