@@ -23,7 +23,10 @@
  *    Data-dependent conditions are never errors: they are per-book counters
  *    (add overflow, trade-log overflow, unknown cancel, malformed message).
  *  - Threads: a context is used by one host thread at a time; one context per
- *    device and process.
+ *    device and process.  Calls on one context must be stream-ordered (one
+ *    stream, or streams joined by events): they share the state buffer and
+ *    the step kernel's two scheduler words, which every launch leaves zeroed.
+ *    Independent contexts (separate state buffers) may run concurrently.
  *  - Layouts: all records are int32 in the paper's field order; counters int64.
  */
 #ifndef LOB_H
