@@ -47,6 +47,21 @@ constexpr int BEST_INVALID = -2, BEST_EMPTY = -1;
 template <int I>
 using IC = std::integral_constant<int, I>;
 
+// Dispatch code of a message (Eq.6 [T, S, Q, P, ...]), computed once per message
+// lane-parallel over a staged chunk and written over T: 0 = padding (T = 0, G21),
+// 1 = malformed (T not in 1..4, S not +-1, cancel/delete Q <= 0, limit P <= 0: G22),
+// else MC_CANCEL | MC_AGGR (limit / market) | MC_MKT (market) | MC_BID (S = +1).
+enum { MC_PAD = 0, MC_BAD = 1, MC_CANCEL = 2, MC_BID = 1, MC_AGGR = 4, MC_MKT = 8 };
+__device__ __forceinline__ int msg_code(const int4 a) {
+    const int T = a.x, S = a.y, Q = a.z, P = a.w;
+    if (T == 0) return MC_PAD;
+    const bool ok_ts = ((unsigned)(T - 1) < 4u) & ((((unsigned)(S + 1)) & ~2u) == 0u);
+    const bool cxl = (unsigned)(T - 2) < 2u;                 // cancel == delete
+    const bool ok = ok_ts && (cxl ? Q > 0 : (T == 4 || P > 0));
+    if (!ok) return MC_BAD;
+    return MC_CANCEL | (S == 1 ? MC_BID : 0) | (cxl ? 0 : MC_AGGR) | (T == 4 ? MC_MKT : 0);
+}
+
 // NEXT row N3 (execution env, Sec.5.1.3 / 5.2): the task shared by all envs
 // and the per-env state (see lob_env.cuh, include/lob.h lob_env_config)
 struct EnvCfg {  // == lob_env_config (include/lob.h)
@@ -314,16 +329,19 @@ struct Engine {
         }
     }
 
-    // Lowest slot whose thread-local predicate holds, or -1: one group minimum of
-    // (row*GT + tid), which is exactly the slot index (interleaved layout).
+    // Lowest slot whose thread-local predicate holds, or a value >= NP (none): one
+    // group minimum of (row*GT + tid), which is exactly the slot index (interleaved
+    // layout).  The select chain picks a constant row (KPL = none), so the slot is
+    // formed once with one multiply-add instead of one add per row.
     template <class Pred>
     __device__ __forceinline__ int lowest(Pred pred) {
-        unsigned loc = 0xffffffffu;
+        unsigned r = KPL;
 #pragma unroll
         for (int j = KPL - 1; j >= 0; --j)
-            if (pred(j)) loc = (unsigned)(j * GT + tid);
-        return (int)gmin_u(loc);
+            if (pred(j)) r = (unsigned)j;
+        return (int)gmin_u(r * GT + (unsigned)tid);
     }
+    static __device__ __forceinline__ bool found(int slot) { return (unsigned)slot < (unsigned)BK::NP; }
 
     // Best(o_s) of side SD over occupied slots: price (ask min / bid max,
     // Eq.5 + G1), then earliest (Ts, Tns), then lowest slot (G4).
@@ -333,23 +351,24 @@ struct Engine {
             recompute_best_multi<SD>();
             return;
         }
-        int lk = INT_MAX;
-        bool has = false;
+        // offset price key (resting prices are >= 1, G22): < 0xffffffff for every
+        // occupied slot, so the all-ones minimum means "side empty" (no vote needed)
+        unsigned lk = 0xffffffffu;
 #pragma unroll
         for (int j = 0; j < KPL; ++j) {
             const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-            const int k = (SD == ASK) ? p : ~p;  // bids: larger price = smaller key
-            if (q > 0) { lk = min(lk, k); has = true; }
+            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+            if (q > 0) lk = min(lk, k);
         }
-        if (!gany(has)) { bslot[SD] = BEST_EMPTY; return; }
-        const int m = gmin_i(has ? lk : INT_MAX);
+        const unsigned m = gmin_u(lk);
+        if (m == 0xffffffffu) { bslot[SD] = BEST_EMPTY; return; }
         // candidates at the best price: thread-local earliest (Ts, Tns, row)
         int lts = INT_MAX, ltns = INT_MAX, lj = -1, lc = 0;
         unsigned lv = 0;
 #pragma unroll
         for (int j = 0; j < KPL; ++j) {
             const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-            const int k = (SD == ASK) ? p : ~p;
+            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
             if (q > 0 && k == m) {
                 const int2 t2 = bk.times(SD, j * GT + tid);
                 if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
@@ -370,7 +389,7 @@ struct Engine {
             slot = (int)gmin_u((in2 && ltns == t2) ? loc : 0xffffffffu);
         }
         bslot[SD] = slot;
-        bP[SD] = (SD == ASK) ? m : ~m;
+        bP[SD] = (SD == ASK) ? (int)(m + 1u) : (int)(INT_MAX - (int)m);
         const int2 bt = bk.times(SD, slot);  // broadcast shared load
         set_bt<SD>(bt.x, bt.y);
     }
@@ -467,13 +486,12 @@ struct Engine {
     // order (OID <= -9000, G12) at the message price.
     template <int SD>
     __device__ __forceinline__ void cancel(int mQ, int mP, int mOID) {
-        if (mQ <= 0) { if (tid == 0) count(ST_BAD, 1); return; }  // G22
         int slot = lowest([&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
-        if (slot < 0)
+        if (!found(slot))
             slot = lowest([&](int j) {
                 return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
             });
-        if (slot < 0) { if (tid == 0) count(ST_UNKNOWN, 1); return; }  // G15
+        if (!found(slot)) { if (tid == 0) count(ST_UNKNOWN, 1); return; }  // G15
         const bool own = tid == (slot & (GT - 1));
         const int j = slot / GT;
         const int qi = bk.get(SD, F_Q, j);
@@ -491,7 +509,6 @@ struct Engine {
     template <int OWN>
     __device__ __forceinline__ void aggress(bool market, int mQ, int mP, int mOID, int mTID, int mTS, int mTNS) {
         constexpr int OPP = 1 - OWN;
-        if (!market && mP <= 0) { if (tid == 0) count(ST_BAD, 1); return; }  // G22
         const int Pa = market ? (OWN == BID ? INT_MAX : 0) : mP;  // P_m = 0 / max_int (G18)
         int Qa = mQ;
         while (Qa > 0) {
@@ -529,7 +546,7 @@ struct Engine {
         }
         // remainder rests as one new order in the lowest empty slot (G3)
         const int slot = lowest([&](int j) { return valid(j) && bk.hot(OWN, F_Q, j) <= 0; });
-        if (slot < 0) {                                              // side saturated (G6)
+        if (!found(slot)) {                                          // side saturated (G6)
             if (tid == 0) { count(ST_ADD_OVF, 1); count(ST_OVF_QTY, Qa); }
             return;
         }
@@ -562,22 +579,26 @@ struct Engine {
         }
     }
 
-    __device__ __forceinline__ void message(const int4 a, const int4 b) {
-        const int T = a.x, S = a.y, Q = a.z, P = a.w;
-        // T in 1..4 and S in {-1, +1}; T = 0 is padding (G21), anything else malformed (G22)
-        const unsigned t1 = (unsigned)(T - 1);
-        if (!((t1 < 4u) & ((((unsigned)(S + 1)) & ~2u) == 0u))) {
-            if (T != 0 && tid == 0) count(ST_BAD, 1);
+    // A message whose first word holds its dispatch code (msg_code) instead of T.
+    __device__ __forceinline__ void message_coded(const int4 a, const int4 b) {
+        const int c = a.x, Q = a.z, P = a.w;
+        if (c < MC_CANCEL) {                                   // padding (G21) / malformed (G22)
+            if (c == MC_BAD && tid == 0) count(ST_BAD, 1);
             return;
         }
         // the paper's 8 (type x side) cases; cancel and delete share one
-        if (t1 - 1u < 2u) {
-            if (S == 1) cancel<BID>(Q, P, b.x);
-            else cancel<ASK>(Q, P, b.x);
+        if (c & MC_AGGR) {
+            if (c & MC_BID) aggress<BID>(c & MC_MKT, Q, P, b.x, b.y, b.z, b.w);
+            else aggress<ASK>(c & MC_MKT, Q, P, b.x, b.y, b.z, b.w);
         } else {
-            if (S == 1) aggress<BID>(T == 4, Q, P, b.x, b.y, b.z, b.w);
-            else aggress<ASK>(T == 4, Q, P, b.x, b.y, b.z, b.w);
+            if (c & MC_BID) cancel<BID>(Q, P, b.x);
+            else cancel<ASK>(Q, P, b.x);
         }
+    }
+    // A message in Eq.6 form (the env agent's own orders).
+    __device__ __forceinline__ void message(int4 a, const int4 b) {
+        a.x = msg_code(a);
+        message_coded(a, b);
     }
 
     // L2 (G23): k-th best distinct price per side and its summed quantity;
@@ -586,31 +607,25 @@ struct Engine {
     template <int SD>
     __device__ __forceinline__ void l2_side(int L, int &outp, int &outq) {
         outp = -1; outq = 0;
-        int key[KPL];
-        bool any = false;
+        // offset price keys as in recompute_best: all-ones = no (further) level
+        unsigned key[KPL];
 #pragma unroll
         for (int j = 0; j < KPL; ++j) {
             const int p = bk.hot(SD, F_P, j);
-            const bool occ = bk.hot(SD, F_Q, j) > 0;
-            key[j] = occ ? ((SD == ASK) ? p : ~p) : INT_MAX;
-            any |= occ;
+            key[j] = bk.hot(SD, F_Q, j) > 0 ? ((SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p)) : 0xffffffffu;
         }
-        bool live = gany(any);
-        for (int k = 0; k < L && live; ++k) {
-            int lk = key[0];
+        for (int k = 0; k < L; ++k) {
+            unsigned lk = key[0];
 #pragma unroll
             for (int j = 1; j < KPL; ++j) lk = min(lk, key[j]);
-            const int m = gmin_i(lk);
+            const unsigned m = gmin_u(lk);
+            if (m == 0xffffffffu) break;
             unsigned lq = 0;
-            bool left = false;
 #pragma unroll
-            for (int j = 0; j < KPL; ++j) {
-                if (key[j] == m) { lq += (unsigned)bk.hot(SD, F_Q, j); key[j] = INT_MAX; }
-                left |= key[j] != INT_MAX;
-            }
+            for (int j = 0; j < KPL; ++j)
+                if (key[j] == m) { lq += (unsigned)bk.hot(SD, F_Q, j); key[j] = 0xffffffffu; }
             const unsigned qs = gadd(lq);
-            if (tid == k) { outp = (SD == ASK) ? m : ~m; outq = (int)qs; }
-            live = gany(left);
+            if (tid == k) { outp = (SD == ASK) ? (int)(m + 1u) : (int)(INT_MAX - (int)m); outq = (int)qs; }
         }
     }
     __device__ __forceinline__ void l2_write(int32_t *dst, int L) {
@@ -849,6 +864,12 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
             mbar_wait(bars + 8 * slot, (seq >> 1) & 1);
             uint32_t maddr = stage + slot * CH * 32;
             int cnt = min(CH, nmsg - c * CH);
+            // decode the chunk lane-parallel: message i's T becomes its dispatch code
+            if (tid < cnt) {
+                const uint32_t m = maddr + 32u * (uint32_t)tid;
+                sts32(m, msg_code(lds128(m)));
+            }
+            group_sync<W>();
             while (cnt > 0) {  // runs up to the next chunk or step end
                 const int run = min(cnt, left);
                 const uint32_t mend = maddr + 32u * run;
@@ -856,11 +877,11 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
                     const int4 a = lds128(maddr), bb = lds128(maddr + 16);
                     if constexpr (ENV) {
                         if (!idle) {
-                            e.message(a, bb);
+                            e.message_coded(a, bb);
                             if (a.x != 0) { last_ts = bb.z; last_tns = bb.w; have_last = true; }
                         }
                     } else {
-                        e.message(a, bb);
+                        e.message_coded(a, bb);
                     }
                     if constexpr (TL1) {
                         e.l1_write(l1dst);
