@@ -303,6 +303,7 @@ def main():
                 "peak_source": peak_src}
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     roofline_issue = None
+    roofline_alu_pipe = None
     if os.path.exists(prof):
         try:
             tr = json.load(open(prof)).get(cfg.name)
@@ -319,6 +320,18 @@ def main():
                                       "unit": "Twarp-instr/s", "frac": ach / peak_issue,
                                       "warp_instructions_per_msg": ipm, "source": tr.get("instr_source"),
                                       "peak_derivation": "148 SMs x 4 schedulers x 1 warp-instr/clk x sm_max_mhz"}
+                # the ALU pipe (ISETP/SEL/LOP3/IADD3/SHF/IMNMX) issues one warp-instruction
+                # every 2 cycles per scheduler: the ceiling that binds first
+                apm = tr.get("alu_pipe_instructions_per_msg")
+                if apm:
+                    peak_alu = 148 * 2 * max_mhz * 1e6 / 1e12
+                    ach = apm * K * cfg.n_msgs / (kmean_ms / 1e3) / 1e12
+                    roofline_alu_pipe = {"bound": "alu", "achieved": ach, "peak": peak_alu,
+                                         "unit": "Twarp-instr/s", "frac": ach / peak_alu,
+                                         "alu_pipe_instructions_per_msg": apm, "source": tr.get("instr_source"),
+                                         "peak_derivation": "148 SMs x 4 schedulers x 0.5 ALU-pipe warp-instr/clk "
+                                                            "(B300_MICROARCH.md: alu rt_SMSP = 2; ncu pct_of_peak agrees) "
+                                                            "x sm_max_mhz"}
         except Exception:
             pass
 
@@ -372,7 +385,7 @@ def main():
                            "profile": cfg.profile, "seed": cfg.seed, "parallelism": f"books sharded x{world}",
                            "l2_flush": "inputs larger than L2 (messages %.2f GB/GPU > 126 MB)"
                                        % (msgs_h.numel() * 4 / 1e9)},
-                "roofline": roofline, "roofline_issue": roofline_issue, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "roofline_issue": roofline_issue, "roofline_alu_pipe": roofline_alu_pipe, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": n_launch, "digest": digest,
                 "clocks": sampler.summary(),
                 "totals": dict(zip(["msgs", "bad", "trades", "trades_dropped", "traded_qty", "cancelled_qty",

@@ -22,6 +22,10 @@ KEYS = [
     "l1tex__t_bytes_pipe_lsu_mem_local_op_ld.sum", "l1tex__t_bytes_pipe_lsu_mem_local_op_st.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__cycles_elapsed.avg.per_second",
     "smsp__warps_eligible.avg.per_cycle_active", "smsp__warps_active.avg.per_cycle_active",
+    "sm__inst_executed_pipe_alu.sum", "sm__inst_executed_pipe_fma.sum", "sm__inst_executed_pipe_lsu.sum",
+    "sm__inst_executed_pipe_cbu.sum", "sm__inst_executed_pipe_adu.sum",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "sm__cycles_active.sum",
 ]
 
 
@@ -57,7 +61,11 @@ def full(rep, msgs=None):
         if msgs:
             try:
                 inst = float(d["smsp__inst_executed.sum"].replace(",", ""))
-                out.append(f"  warp-instructions per message: {inst / msgs:.1f}")
+                out.append(f"  warp-instructions per message: {inst / msgs:.2f}")
+                for pipe in ("alu", "fma", "lsu", "cbu", "adu"):
+                    k = f"sm__inst_executed_pipe_{pipe}.sum"
+                    if k in d:
+                        out.append(f"  {pipe}-pipe warp-instructions per message: {float(d[k].replace(',', '')) / msgs:.2f}")
                 rd = float(d["dram__bytes_read.sum"].replace(",", "")) * (1 if units[hdr.index("dram__bytes_read.sum")] == "byte" else 1)
                 out.append(f"  (dram units: {units[hdr.index('dram__bytes_read.sum')]})")
             except (KeyError, ValueError):
