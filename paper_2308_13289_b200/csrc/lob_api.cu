@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 
 #include "../../include/lob.h"
@@ -76,6 +77,7 @@ struct lob_ctx {
     int sm_count;
     Geo geo;
     int grid_cap[4];  // persistent grid: resident CTAs of the step kernel, per MODE
+    bool force_wide;  // test hook (env LOB_FORCE_WIDE=1): MODE 3 for every 4-row batch
     int32_t *book() const { return reinterpret_cast<int32_t *>(state + lay.off_book); }
     int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
     int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
@@ -136,7 +138,7 @@ int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M,
         const unsigned need = blocks_for(nb, G);
         constexpr bool kWide = KPL == 4 && W == 1;  // MODE 3 exists for 4-row warp books only
         // many waves of books: the 8-CTA/SM build (occupancy beats its extra spills)
-        const bool wide = kWide && !env && !d_l1 && (long long)nb >= 8LL * ctx->grid_cap[0] * G;
+        const bool wide = kWide && !env && !d_l1 && (ctx->force_wide || (long long)nb >= 8LL * ctx->grid_cap[0] * G);
         const unsigned cap = (unsigned)ctx->grid_cap[env ? 2 : (d_l1 ? 1 : (wide ? 3 : 0))];
         const unsigned grid = need < cap ? need : cap;
         const int smem = step_smem_bytes<KPL, W, G>();
@@ -183,6 +185,10 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
     c->state = static_cast<char *>(d_state);
     c->sm_count = sms;
     c->geo = geo_of(cfg->capacity);
+    {
+        const char *fw = getenv("LOB_FORCE_WIDE");
+        c->force_wide = fw && fw[0] == '1';
+    }
     int per_sm[4] = {1, 1, 1, 1};
     int rc = LOB_OK;
     for_geo(c->geo, [&](auto kc, auto wc, auto gc) {

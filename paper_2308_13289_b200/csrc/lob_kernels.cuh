@@ -255,7 +255,7 @@ struct RegBook {
 };
 
 // ------------------------------------------------------------------ the engine
-template <class BK, bool TL1 = false>
+template <class BK, bool TL1 = false, bool ROWS = false>
 struct Engine {
     static constexpr int KPL = BK::KPL, W = BK::W, GT = BK::GT;
     BK bk;
@@ -270,6 +270,7 @@ struct Engine {
     // shared memory for warp books (saves 4 registers on the 72-register kernel)
     static constexpr bool kBtRegs = (W > 1);
     int bTS[2], bTNS[2];
+    int hr[2];              // row high-water mark per side (see with_rows)
     unsigned bV[2];         // TL1: total quantity at the cached best price (its L1 volume)
     long long part_cxl;     // cancelled quantity, accumulated on the owner thread (G14)
     long long part_trd;     // traded quantity, accumulated on the owner thread
@@ -343,6 +344,68 @@ struct Engine {
     }
     static __device__ __forceinline__ bool found(int slot) { return (unsigned)slot < (unsigned)BK::NP; }
 
+    // Row high-water mark: every occupied slot of side s lies in rows 0..hr[s] (-1: no
+    // order).  Orders take the lowest empty slot (G3), so a book of n orders fills the
+    // low rows; a scan over occupied slots runs over the first R rows only, R the
+    // smallest of {2, 4, KPL} above hr (one uniform branch; rows between hr and R are
+    // empty, so scanning them is harmless).  Raised on every add, lowered to the exact
+    // value at every L2 snapshot.
+    // ROWS = false (latency-bound launches: one wave of few books): always all rows --
+    // the branch costs more latency than the skipped rows save (C2: -4 %).
+    template <class F>
+    __device__ __forceinline__ void with_rows(int h, F &&f) {
+        if constexpr (KPL <= 2 || !ROWS) {
+            f(IC<KPL>{});
+        } else if constexpr (KPL <= 4) {
+            if (h < 2) f(IC<2>{});
+            else f(IC<KPL>{});
+        } else {
+            if (h < 2) f(IC<2>{});
+            else if (h < 4) f(IC<4>{});
+            else f(IC<KPL>{});
+        }
+    }
+    // highest occupied row of side s (group-uniform), -1 if none
+    template <int SD>
+    __device__ __forceinline__ int top_row() {
+        int hl = -1;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j)
+            if (bk.hot(SD, F_Q, j) > 0) hl = j;
+        return (KPL - 1) - (int)gmin_u((unsigned)(KPL - 1 - hl));
+    }
+    __device__ __forceinline__ void init_rows() {
+        if constexpr (ROWS) {
+            hr[ASK] = top_row<ASK>();
+            hr[BID] = top_row<BID>();
+        } else {
+            hr[ASK] = hr[BID] = KPL - 1;
+        }
+    }
+    // lowest occupied slot (pred includes Q > 0) on side SD, or >= NP
+    template <int SD, class Pred>
+    __device__ __forceinline__ int lowest_occ(Pred pred) {
+        unsigned r = KPL;
+        with_rows(hr[SD], [&](auto R) {
+#pragma unroll
+            for (int j = R - 1; j >= 0; --j)
+                if (pred(j)) r = (unsigned)j;
+        });
+        return (int)gmin_u(r * GT + (unsigned)tid);
+    }
+    // lowest empty slot < N on side SD (G3), or >= NP: rows 0..R-1, else row R (empty)
+    template <int SD>
+    __device__ __forceinline__ int lowest_free() {
+        unsigned r = KPL;
+        with_rows(hr[SD], [&](auto R) {
+            if constexpr (R < KPL) r = valid(R) ? (unsigned)R : (unsigned)KPL;
+#pragma unroll
+            for (int j = R - 1; j >= 0; --j)
+                if (valid(j) && bk.hot(SD, F_Q, j) <= 0) r = (unsigned)j;
+        });
+        return (int)gmin_u(r * GT + (unsigned)tid);
+    }
+
     // Best(o_s) of side SD over occupied slots: price (ask min / bid max,
     // Eq.5 + G1), then earliest (Ts, Tns), then lowest slot (G4).
     template <int SD>
@@ -354,28 +417,32 @@ struct Engine {
         // offset price key (resting prices are >= 1, G22): < 0xffffffff for every
         // occupied slot, so the all-ones minimum means "side empty" (no vote needed)
         unsigned lk = 0xffffffffu;
+        with_rows(hr[SD], [&](auto R) {
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
-            if (q > 0) lk = min(lk, k);
-        }
+            for (int j = 0; j < R; ++j) {
+                const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+                const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+                if (q > 0) lk = min(lk, k);
+            }
+        });
         const unsigned m = gmin_u(lk);
         if (m == 0xffffffffu) { bslot[SD] = BEST_EMPTY; return; }
         // candidates at the best price: thread-local earliest (Ts, Tns, row)
         int lts = INT_MAX, ltns = INT_MAX, lj = -1, lc = 0;
         unsigned lv = 0;
+        with_rows(hr[SD], [&](auto R) {
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
-            if (q > 0 && k == m) {
-                const int2 t2 = bk.times(SD, j * GT + tid);
-                if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
-                ++lc;
-                lv += (unsigned)q;
+            for (int j = 0; j < R; ++j) {
+                const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+                const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+                if (q > 0 && k == m) {
+                    const int2 t2 = bk.times(SD, j * GT + tid);
+                    if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
+                    ++lc;
+                    lv += (unsigned)q;
+                }
             }
-        }
+        });
         if constexpr (TL1) bV[SD] = gadd(lv);
         const unsigned loc = lj < 0 ? 0xffffffffu : (unsigned)(lj * GT + tid);
         int slot;
@@ -401,26 +468,30 @@ struct Engine {
     template <int SD>
     __device__ __forceinline__ void recompute_best_multi() {
         unsigned lk = 0xffffffffu;
+        with_rows(hr[SD], [&](auto R) {
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
-            if (q > 0) lk = min(lk, k);
-        }
+            for (int j = 0; j < R; ++j) {
+                const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+                const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+                if (q > 0) lk = min(lk, k);
+            }
+        });
         const unsigned m = gmin_u(lk);
         if (m == 0xffffffffu) { bslot[SD] = BEST_EMPTY; return; }
         int lts = INT_MAX, ltns = INT_MAX, lj = -1;
         unsigned lv = 0;
+        with_rows(hr[SD], [&](auto R) {
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
-            if (q > 0 && k == m) {
-                const int2 t2 = bk.times(SD, j * GT + tid);
-                if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
-                lv += (unsigned)q;
+            for (int j = 0; j < R; ++j) {
+                const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+                const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+                if (q > 0 && k == m) {
+                    const int2 t2 = bk.times(SD, j * GT + tid);
+                    if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
+                    lv += (unsigned)q;
+                }
             }
-        }
+        });
         if constexpr (TL1) bV[SD] = gadd(lv);
         const bool in = lj >= 0;
         const int w1 = __reduce_min_sync(FULL, in ? lts : INT_MAX);
@@ -486,9 +557,9 @@ struct Engine {
     // order (OID <= -9000, G12) at the message price.
     template <int SD>
     __device__ __forceinline__ void cancel(int mQ, int mP, int mOID) {
-        int slot = lowest([&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
+        int slot = lowest_occ<SD>([&](auto j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
         if (!found(slot))
-            slot = lowest([&](int j) {
+            slot = lowest_occ<SD>([&](auto j) {
                 return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
             });
         if (!found(slot)) { if (tid == 0) count(ST_UNKNOWN, 1); return; }  // G15
@@ -545,12 +616,13 @@ struct Engine {
             return;
         }
         // remainder rests as one new order in the lowest empty slot (G3)
-        const int slot = lowest([&](int j) { return valid(j) && bk.hot(OWN, F_Q, j) <= 0; });
+        const int slot = lowest_free<OWN>();
         if (!found(slot)) {                                          // side saturated (G6)
             if (tid == 0) { count(ST_ADD_OVF, 1); count(ST_OVF_QTY, Qa); }
             return;
         }
         const bool own = tid == (slot & (GT - 1));
+        if constexpr (ROWS) hr[OWN] = max(hr[OWN], slot / GT);
         bk.row(slot / GT, [&](auto J) {                              // G27
             if (own) {
                 bk.v[OWN][F_P][J] = mP;
@@ -604,29 +676,40 @@ struct Engine {
     // L2 (G23): k-th best distinct price per side and its summed quantity;
     // thread k keeps level k.  Absent levels are (-1, 0).  Each level takes the
     // group minimum of the remaining keys and retires every slot at that price.
-    template <int SD>
-    __device__ __forceinline__ void l2_side(int L, int &outp, int &outq) {
-        outp = -1; outq = 0;
+    template <int SD, int R>
+    __device__ __forceinline__ void l2_rows(int L, int &outp, int &outq) {
         // offset price keys as in recompute_best: all-ones = no (further) level
-        unsigned key[KPL];
+        unsigned key[R];
+        int hl = -1;
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) {
+        for (int j = 0; j < R; ++j) {
             const int p = bk.hot(SD, F_P, j);
-            key[j] = bk.hot(SD, F_Q, j) > 0 ? ((SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p)) : 0xffffffffu;
+            const bool occ = bk.hot(SD, F_Q, j) > 0;
+            key[j] = occ ? ((SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p)) : 0xffffffffu;
+            if (occ) hl = j;
         }
+        if constexpr (ROWS) hr[SD] = (KPL - 1) - (int)gmin_u((unsigned)(KPL - 1 - hl));  // exact row bound again
         for (int k = 0; k < L; ++k) {
             unsigned lk = key[0];
 #pragma unroll
-            for (int j = 1; j < KPL; ++j) lk = min(lk, key[j]);
+            for (int j = 1; j < R; ++j) lk = min(lk, key[j]);
             const unsigned m = gmin_u(lk);
             if (m == 0xffffffffu) break;
             unsigned lq = 0;
 #pragma unroll
-            for (int j = 0; j < KPL; ++j)
+            for (int j = 0; j < R; ++j)
                 if (key[j] == m) { lq += (unsigned)bk.hot(SD, F_Q, j); key[j] = 0xffffffffu; }
             const unsigned qs = gadd(lq);
             if (tid == k) { outp = (SD == ASK) ? (int)(m + 1u) : (int)(INT_MAX - (int)m); outq = (int)qs; }
         }
+    }
+    // L2 over the first R rows only (with_rows)
+    template <int SD>
+    __device__ __forceinline__ void l2_side(int L, int &outp, int &outq) {
+        outp = -1; outq = 0;
+        const int h = hr[SD];
+        if (h < 0) return;
+        with_rows(h, [&](auto R) { l2_rows<SD, R>(L, outp, outq); });
     }
     __device__ __forceinline__ void l2_write(int32_t *dst, int L) {
         int ap, aq, bp, bq;
@@ -797,6 +880,10 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
     lob_step(const Params p, const EnvParams ep) {
     using BK = RegBook<KPL, W>;
     constexpr bool TL1 = MODE == 1, ENV = MODE == 2;
+    // row-bounded scans (Engine::with_rows) for throughput launches: many-wave 4-row
+    // books (MODE 3, C4 +4.5 %) and multi-warp books (C5 N = 2048 +9 %); measured slower
+    // for one-warp 8-row books (C5 N = 256 -3 %) and few-wave 4-row launches (C2 -4 %)
+    constexpr bool kRows = MODE == 3 || W > 1;
     extern __shared__ __align__(128) unsigned char dyn[];
     const int g = threadIdx.x / (32 * W);
     const int tid = (int)opaque(threadIdx.x % (32 * W));
@@ -839,12 +926,13 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
             }
         }
         if (tid < NST) sts64(scratch + 8u * tid, 0);
-        Engine<BK, TL1> e(p);
+        Engine<BK, TL1, kRows> e(p);
         e.bk.cold = cold;
         e.bk.tid = tid;
         e.tid = tid; e.book = b; e.ntr = 0; e.sc = scratch; e.xph = 0;
         e.part_cxl = 0; e.part_trd = 0;
         e.bk.load(p.book + (size_t)b * 2 * NF * BK::NP);
+        e.init_rows();
         e.bslot[0] = e.bslot[1] = BEST_INVALID;
         e.bP[0] = e.bP[1] = 0;
         e.bV[0] = e.bV[1] = 0;
@@ -1116,6 +1204,7 @@ __global__ void __launch_bounds__(32 * W) lob_export_l2(const int32_t *book, int
     e.bk.cold = smem_u32(dyn);
     e.sc = smem_u32(dyn + 2 * BK::NP * 16);
     e.bk.load(book + (size_t)b * 2 * NF * BK::NP);
+    e.init_rows();
     e.l2_write(out + (size_t)b * L * 4, L);
 }
 template <int KPL, int W>

@@ -72,6 +72,19 @@ def test_geometry_boundaries(N):
         assert_outputs_equal(g, o, what=f"{profile} N={N}")
 
 
+@pytest.mark.parametrize("profile,N,calls", [("ties", 100, 1), ("overflow", 100, 1), ("synthetic", 100, 3),
+                                             ("garbage", 128, 1), ("heavy_market", 97, 2), ("cancel_heavy", 100, 7),
+                                             ("lobster", 120, 1)])
+def test_wide_build_row_bounds(monkeypatch, profile, N, calls):
+    # the many-wave build (MODE 3: row-bounded scans, Engine::with_rows) forced on a
+    # small batch of 4-row books: overflowing, tied, malformed and sweeping streams
+    # move the row high-water mark up to the last (partial) row and back down
+    monkeypatch.setenv("LOB_FORCE_WIDE", "1")
+    cfg = lobgen.Config("w", 700, N, 8, 40, min(N, 40), 64, 10, profile, 3 * N + calls)
+    g, o = _both(cfg, calls=calls)
+    assert_outputs_equal(g, o, what=f"wide {profile} N={N} calls={calls}")
+
+
 @pytest.mark.parametrize("L,Tcap", [(1, 0), (32, 3), (10, 1)])
 def test_levels_and_tiny_trade_log(L, Tcap):
     cfg = lobgen.Config("p", 200, 100, 5, 50, 40, Tcap, L, "heavy_market", 5)
