@@ -222,6 +222,20 @@ struct RegBook {
         for (int jj = 0; jj < KPL_; ++jj)
             if (pred && j == jj) v[s][f][jj] = x;
     }
+    // the same for a row known to be below R (shorter select chains)
+    template <int R>
+    __device__ __forceinline__ int32_t get_r(int s, int f, int j) const {
+        int32_t r = v[s][f][0];
+#pragma unroll
+        for (int jj = 1; jj < R; ++jj) r = (j == jj) ? v[s][f][jj] : r;
+        return r;
+    }
+    template <int R>
+    __device__ __forceinline__ void put_if_r(bool pred, int s, int f, int j, int32_t x) {
+#pragma unroll
+        for (int jj = 0; jj < R; ++jj)
+            if (pred && j == jj) v[s][f][jj] = x;
+    }
     __device__ __forceinline__ void load(const int32_t *g) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
@@ -565,10 +579,13 @@ struct Engine {
         if (!found(slot)) { if (tid == 0) count(ST_UNKNOWN, 1); return; }  // G15
         const bool own = tid == (slot & (GT - 1));
         const int j = slot / GT;
-        const int qi = bk.get(SD, F_Q, j);
-        const int cq = (mQ < qi) ? mQ : qi;
-        if (own) part_cxl += cq;                   // G14
-        bk.put_if(own, SD, F_Q, j, qi - mQ);       // Q <= 0 -> empty
+        int cq;
+        with_rows(hr[SD], [&](auto R) {            // the slot is occupied: its row is below R
+            const int qi = bk.template get_r<R>(SD, F_Q, j);
+            cq = (mQ < qi) ? mQ : qi;
+            if (own) part_cxl += cq;               // G14
+            bk.template put_if_r<R>(own, SD, F_Q, j, qi - mQ);  // Q <= 0 -> empty
+        });
         if constexpr (TL1) {                       // the level volume loses what was cancelled there
             const int d = bcast(bk.get(SD, F_P, j) == bP[SD] ? cq : 0, slot & (GT - 1));
             if (bslot[SD] >= 0) bV[SD] -= (unsigned)d;
