@@ -114,14 +114,24 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ unsigned mbar_try(uint32_t bar, uint32_t parity) {
+    unsigned ok;
     asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "LAB_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
         : "memory");
+    return ok;
+}
+// every thread of the warp waits for the phase; the loop condition is a warp reduction,
+// so ptxas sees a uniform loop (a per-thread spin would leave the warp "possibly
+// diverged" for its convergence analysis: reconvergence barriers and divergence checks
+// around every later branch and collective)
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    while (__reduce_min_sync(0xffffffffu, mbar_try(bar, parity)) == 0u) {
+    }
 }
 // 1-D bulk copy global -> shared (TMA bulk engine), completes tx bytes on `bar`
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
@@ -902,14 +912,18 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
     // for one-warp 8-row books (C5 N = 256 -3 %) and few-wave 4-row launches (C2 -4 %)
     constexpr bool kRows = MODE == 3 || W > 1;
     extern __shared__ __align__(128) unsigned char dyn[];
-    const int g = threadIdx.x / (32 * W);
+    // the group index through a warp reduction: ptxas then knows it (and every shared
+    // address below) is warp-uniform, so messages loaded from those addresses are
+    // uniform and the dispatch branches need no reconvergence (BSSY/BSYNC) and the
+    // warp collectives no divergence check (BRA.DIV)
+    const int g = G == 1 ? 0 : (int)__reduce_min_sync(FULL, threadIdx.x / (32 * W));
     const int tid = (int)opaque(threadIdx.x % (32 * W));
     // carve this group's region: stage [2][CH][32 B] | bars [2] | cold [2][NP][16 B] | scratch
     unsigned char *base = dyn + g * (step_smem_bytes<KPL, W, G>() / G);
-    const uint32_t stage = opaque(smem_u32(base));
-    const uint32_t bars = opaque(smem_u32(base + 2 * CH * 32));
-    const uint32_t cold = opaque(smem_u32(base + 2 * CH * 32 + 16));
-    const uint32_t scratch = opaque(smem_u32(base + 2 * CH * 32 + 16 + 2 * BK::NP * 16));
+    const uint32_t stage = smem_u32(base);
+    const uint32_t bars = smem_u32(base + 2 * CH * 32);
+    const uint32_t cold = smem_u32(base + 2 * CH * 32 + 16);
+    const uint32_t scratch = smem_u32(base + 2 * CH * 32 + 16 + 2 * BK::NP * 16);
     if (tid == 0) {
         mbar_init(bars, 1);
         mbar_init(bars + 8, 1);
@@ -921,7 +935,7 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
     uint32_t chunk_seq = 0;
     // dynamic book scheduling: deep sweeps make books unequal, so after its first
     // (static) book a group takes the next one from a global counter when it is free
-    const uint32_t next_addr = scratch + 8u * NST + 16u + (W == 1 ? 8u : 32u * W);
+    constexpr int next_off = 2 * CH * 32 + 16 + 2 * BK::NP * 16 + 8 * NST + 16 + (W == 1 ? 8 : 32 * W);
     const int groups = gridDim.x * G;
     const bool multi = groups < p.nb;  // more books than groups: dynamic scheduling (sched counters)
     int lb = blockIdx.x * G + g;
@@ -1038,15 +1052,16 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
         if (tid == 0) p.ntrades[b] = logged;
         if constexpr (ENV) env_post<W>(p, ep, b, tid, logged, have_last, last_ts, last_tns);
         if (!multi) break;  // one wave: every book had a group of its own
-        int next = 0;
-        if (tid == 0) next = groups + (int)atomicAdd(p.sched, 1u);
-        if constexpr (W == 1) {
-            lb = __shfl_sync(FULL, next, 0);
-        } else {
-            if (tid == 0) sts32(next_addr, next);
-            __syncthreads();
-            lb = lds32(next_addr);
-        }
+        // the next book: claimed by thread 0 with an atomic, handed to the group through a
+        // plain shared-memory word.  An atomic's result counts as thread-divergent in the
+        // compiler's uniformity analysis (and a shuffle or reduction of it stays so), which
+        // would make the whole persistent loop "possibly diverged": reconvergence barriers
+        // around every branch and a divergence check before every warp collective (~2x
+        // the control instructions).  A load from a uniform shared address is uniform.
+        int *next_word = reinterpret_cast<int *>(base + next_off);
+        if (tid == 0) *next_word = groups + (int)atomicAdd(p.sched, 1u);
+        group_sync<W>();
+        lb = *next_word;
     }
     // the last group to finish re-arms the counters for the next launch
     if (multi && tid == 0) {
