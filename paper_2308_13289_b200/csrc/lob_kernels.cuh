@@ -907,10 +907,10 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
     lob_step(const Params p, const EnvParams ep) {
     using BK = RegBook<KPL, W>;
     constexpr bool TL1 = MODE == 1, ENV = MODE == 2;
-    // row-bounded scans (Engine::with_rows) for throughput launches: many-wave 4-row
-    // books (MODE 3, C4 +4.5 %) and multi-warp books (C5 N = 2048 +9 %); measured slower
-    // for one-warp 8-row books (C5 N = 256 -3 %) and few-wave 4-row launches (C2 -4 %)
-    constexpr bool kRows = MODE == 3 || W > 1;
+    // row-bounded scans (Engine::with_rows) in every build: C4 +4.5 %, C3 +10 %, C5
+    // N = 256 +3 %, N = 2048 +9 %, C2 -0.5 % (measured with the uniform persistent loop;
+    // before it, the extra branch cost C2 4 %)
+    constexpr bool kRows = true;
     extern __shared__ __align__(128) unsigned char dyn[];
     // the group index through a warp reduction: ptxas then knows it (and every shared
     // address below) is warp-uniform, so messages loaded from those addresses are
