@@ -78,6 +78,8 @@ struct lob_ctx {
     Geo geo;
     int grid_cap[4];  // persistent grid: resident CTAs of the step kernel, per MODE
     bool force_wide;  // test hook (env LOB_FORCE_WIDE=1): MODE 3 for every 4-row batch
+    int grid_limit;   // test hook (env LOB_GRID_CAP=n): at most n CTAs per step launch, so
+                      // small batches exercise the dynamic book scheduler
     int32_t *book() const { return reinterpret_cast<int32_t *>(state + lay.off_book); }
     int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
     int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
@@ -140,7 +142,8 @@ int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M,
         // many waves of books: the 8-CTA/SM build (occupancy beats its extra spills)
         const bool wide = kWide && !env && !d_l1 && (ctx->force_wide || (long long)nb >= 8LL * ctx->grid_cap[0] * G);
         const unsigned cap = (unsigned)ctx->grid_cap[env ? 2 : (d_l1 ? 1 : (wide ? 3 : 0))];
-        const unsigned grid = need < cap ? need : cap;
+        unsigned grid = need < cap ? need : cap;
+        if (ctx->grid_limit > 0 && grid > (unsigned)ctx->grid_limit) grid = (unsigned)ctx->grid_limit;
         const int smem = step_smem_bytes<KPL, W, G>();
         if (env) lob_step<KPL, W, G, 2><<<grid, 32 * W * G, smem, st>>>(p, ep);
         else if (d_l1) lob_step<KPL, W, G, 1><<<grid, 32 * W * G, smem, st>>>(p, ep);
@@ -188,6 +191,8 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
     {
         const char *fw = getenv("LOB_FORCE_WIDE");
         c->force_wide = fw && fw[0] == '1';
+        const char *gc = getenv("LOB_GRID_CAP");
+        c->grid_limit = gc ? atoi(gc) : 0;
     }
     int per_sm[4] = {1, 1, 1, 1};
     int rc = LOB_OK;

@@ -1,0 +1,11 @@
+#!/bin/bash
+# compute-sanitizer over scripts/sanitize.py: default grid, and a 1-CTA grid (LOB_GRID_CAP=1)
+# so the dynamic book scheduler's shared-word hand-off runs under racecheck/synccheck.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck; do
+  for cap in 0 1; do
+    LOB_GRID_CAP=$cap timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize.py > gpurun_out/san_${tool}_cap$cap.txt 2>&1
+    echo "$tool cap=$cap rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|hazard' gpurun_out/san_${tool}_cap$cap.txt | tail -1)"
+  done
+done

@@ -85,6 +85,21 @@ def test_wide_build_row_bounds(monkeypatch, profile, N, calls):
     assert_outputs_equal(g, o, what=f"wide {profile} N={N} calls={calls}")
 
 
+@pytest.mark.parametrize("N,cap,wide,calls", [(100, 1, False, 1), (100, 3, True, 4), (33, 2, False, 2),
+                                             (200, 5, False, 1), (512, 3, False, 2), (1024, 2, False, 1)])
+def test_dynamic_scheduling_small_grid(monkeypatch, N, cap, wide, calls):
+    # LOB_GRID_CAP caps the persistent grid, so a few hundred books run through the
+    # dynamic book scheduler (atomic claim + shared-word hand-off, counter re-arm
+    # between launches) in every geometry and in the many-wave build
+    monkeypatch.setenv("LOB_GRID_CAP", str(cap))
+    if wide:
+        monkeypatch.setenv("LOB_FORCE_WIDE", "1")
+    K = 150 if N >= 512 else 400
+    cfg = lobgen.Config("dyn", K, N, 4, 30, min(N, 20), 32, 10, "heavy_market" if N < 512 else "lobster", N + cap)
+    g, o = _both(cfg, calls=calls)
+    assert_outputs_equal(g, o, what=f"dyn N={N} cap={cap} wide={wide} calls={calls}")
+
+
 @pytest.mark.parametrize("L,Tcap", [(1, 0), (32, 3), (10, 1)])
 def test_levels_and_tiny_trade_log(L, Tcap):
     cfg = lobgen.Config("p", 200, 100, 5, 50, 40, Tcap, L, "heavy_market", 5)
