@@ -202,10 +202,12 @@ def test_host_path_equals_device_path():
     assert torch.equal(b.book(), a.book())
 
 
-def test_full_size_c4_sampled_books():
-    """C4 at BASELINE.json's full size (65,536 books) in the launch configuration
-    bench.py times; sampled books are recomputed one by one by the oracle."""
-    cfg = lobgen.CONFIGS["C4"]
+@pytest.mark.parametrize("name", ["C4", "C3", "C5_32", "C5_100", "C5_512", "C5_2048"])
+def test_full_size_sampled_books(name):
+    """Every BASELINE.json config at its full size (C4: 65,536 books, the launch
+    configuration bench.py times; C3: 16,384; C5: 4,096 at each capacity), sampled
+    books recomputed one by one by the oracle."""
+    cfg = lobgen.CONFIGS[name]
     msgs, init = lobgen.generate(cfg)
     e = GpuEngine(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
     g = run_engine(e, cfg, msgs, init, lobgen.INIT_TS, lobgen.INIT_TNS)
@@ -215,7 +217,7 @@ def test_full_size_c4_sampled_books():
     want = run_engine(o, cfg, np.ascontiguousarray(msgs[sample]), np.ascontiguousarray(init[sample]),
                       lobgen.INIT_TS, lobgen.INIT_TNS)
     got = {k: v[sample] for k, v in g.items()}
-    assert_outputs_equal(got, want, what="C4 full-size sample")
+    assert_outputs_equal(got, want, what=f"{name} full-size sample")
     from digest import state_digest
     dg = e.b.digest().cpu().numpy().view(np.uint64)
     np.testing.assert_array_equal(dg[sample], state_digest(want["book"], want["trades"], want["n_trades"],
