@@ -85,6 +85,10 @@ size_t lob_state_bytes(const lob_config *cfg);
  * LOB_EUNSUPPORTED for capacity > LOB_MAX_CAPACITY, LOB_ECUDA if the device
  * cannot be queried. */
 int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state);
+/* Test hooks, read from the environment by lob_create (results never change, only
+ * the launch shape): LOB_FORCE_WIDE=1 launches the many-wave build of the step
+ * kernel for every 4-row batch; LOB_GRID_CAP=n caps the persistent grid at n CTAs,
+ * so small batches run through the dynamic book scheduler. */
 void lob_destroy(lob_ctx *ctx); /* frees the host handle only */
 
 /* a0: book init.  Both sides and the trade log become -1
