@@ -406,6 +406,15 @@ struct Engine {
             hr[ASK] = hr[BID] = KPL - 1;
         }
     }
+    // lowest slot of rows 0..R-1 whose predicate holds, or >= NP
+    template <int R, class Pred>
+    __device__ __forceinline__ int lowest_rows(Pred pred) {
+        unsigned r = KPL;
+#pragma unroll
+        for (int j = R - 1; j >= 0; --j)
+            if (pred(j)) r = (unsigned)j;
+        return (int)gmin_u(r * GT + (unsigned)tid);
+    }
     // lowest occupied slot (pred includes Q > 0) on side SD, or >= NP
     template <int SD, class Pred>
     __device__ __forceinline__ int lowest_occ(Pred pred) {
@@ -581,21 +590,23 @@ struct Engine {
     // order (OID <= -9000, G12) at the message price.
     template <int SD>
     __device__ __forceinline__ void cancel(int mQ, int mP, int mOID) {
-        int slot = lowest_occ<SD>([&](auto j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
+        // one row-bound branch for the whole cancel: scans and owner update over R rows
+        with_rows(hr[SD], [&](auto R) { cancel_r<SD, R>(mQ, mP, mOID); });
+    }
+    template <int SD, int R>
+    __device__ __forceinline__ void cancel_r(int mQ, int mP, int mOID) {
+        int slot = lowest_rows<R>([&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
         if (!found(slot))
-            slot = lowest_occ<SD>([&](auto j) {
+            slot = lowest_rows<R>([&](int j) {
                 return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
             });
         if (!found(slot)) { if (tid == 0) count(ST_UNKNOWN, 1); return; }  // G15
         const bool own = tid == (slot & (GT - 1));
-        const int j = slot / GT;
-        int cq;
-        with_rows(hr[SD], [&](auto R) {            // the slot is occupied: its row is below R
-            const int qi = bk.template get_r<R>(SD, F_Q, j);
-            cq = (mQ < qi) ? mQ : qi;
-            if (own) part_cxl += cq;               // G14
-            bk.template put_if_r<R>(own, SD, F_Q, j, qi - mQ);  // Q <= 0 -> empty
-        });
+        const int j = slot / GT;                   // the slot is occupied: its row is below R
+        const int qi = bk.template get_r<R>(SD, F_Q, j);
+        const int cq = (mQ < qi) ? mQ : qi;
+        if (own) part_cxl += cq;                   // G14
+        bk.template put_if_r<R>(own, SD, F_Q, j, qi - mQ);  // Q <= 0 -> empty
         if constexpr (TL1) {                       // the level volume loses what was cancelled there
             const int d = bcast(bk.get(SD, F_P, j) == bP[SD] ? cq : 0, slot & (GT - 1));
             if (bslot[SD] >= 0) bV[SD] -= (unsigned)d;
@@ -687,10 +698,10 @@ struct Engine {
         }
         // the paper's 8 (type x side) cases; cancel and delete share one
         if (c & MC_AGGR) {
-            if (c & MC_BID) aggress<BID>(c & MC_MKT, Q, P, b.x, b.y, b.z, b.w);
+            if ((c & MC_BID) != 0) aggress<BID>(c & MC_MKT, Q, P, b.x, b.y, b.z, b.w);
             else aggress<ASK>(c & MC_MKT, Q, P, b.x, b.y, b.z, b.w);
         } else {
-            if (c & MC_BID) cancel<BID>(Q, P, b.x);
+            if ((c & MC_BID) != 0) cancel<BID>(Q, P, b.x);
             else cancel<ASK>(Q, P, b.x);
         }
     }
