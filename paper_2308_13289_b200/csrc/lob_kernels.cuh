@@ -220,6 +220,16 @@ struct RegBook {
             }
         }
     }
+    // f(row) for a uniform row j known to be below RR: a compare chain, no jump table
+    template <int RR, int J0 = 0, class F>
+    __device__ __forceinline__ void row_r(int j, F &&f) {
+        if constexpr (J0 + 1 >= RR) {
+            f(IC<J0>{});
+        } else {
+            if (j == J0) f(IC<J0>{});
+            else row_r<RR, J0 + 1>(j, f);
+        }
+    }
     // value of field f in row j (uniform j), branch-free select chain
     __device__ __forceinline__ int32_t get(int s, int f, int j) const {
         int32_t r = v[s][f][0];
@@ -426,19 +436,6 @@ struct Engine {
         });
         return (int)gmin_u(r * GT + (unsigned)tid);
     }
-    // lowest empty slot < N on side SD (G3), or >= NP: rows 0..R-1, else row R (empty)
-    template <int SD>
-    __device__ __forceinline__ int lowest_free() {
-        unsigned r = KPL;
-        with_rows(hr[SD], [&](auto R) {
-            if constexpr (R < KPL) r = valid(R) ? (unsigned)R : (unsigned)KPL;
-#pragma unroll
-            for (int j = R - 1; j >= 0; --j)
-                if (valid(j) && bk.hot(SD, F_Q, j) <= 0) r = (unsigned)j;
-        });
-        return (int)gmin_u(r * GT + (unsigned)tid);
-    }
-
     // Best(o_s) of side SD over occupied slots: price (ask min / bid max,
     // Eq.5 + G1), then earliest (Ts, Tns), then lowest slot (G4).
     template <int SD>
@@ -654,20 +651,33 @@ struct Engine {
             return;
         }
         // remainder rests as one new order in the lowest empty slot (G3)
-        const int slot = lowest_free<OWN>();
+        with_rows(hr[OWN], [&](auto R) { add_r<OWN, R>(Qa, mP, mOID, mTID, mTS, mTNS); });
+    }
+    // the add over the row bound R: free slot in rows 0..R-1, else row R's first slot
+    template <int OWN, int R>
+    __device__ __forceinline__ void add_r(int Qa, int mP, int mOID, int mTID, int mTS, int mTNS) {
+        unsigned r = KPL;
+        if constexpr (R < KPL) r = valid(R) ? (unsigned)R : (unsigned)KPL;
+#pragma unroll
+        for (int j = R - 1; j >= 0; --j)
+            if (valid(j) && bk.hot(OWN, F_Q, j) <= 0) r = (unsigned)j;
+        const int slot = (int)gmin_u(r * GT + (unsigned)tid);
         if (!found(slot)) {                                          // side saturated (G6)
             if (tid == 0) { count(ST_ADD_OVF, 1); count(ST_OVF_QTY, Qa); }
             return;
         }
         const bool own = tid == (slot & (GT - 1));
         if constexpr (ROWS) hr[OWN] = max(hr[OWN], slot / GT);
-        bk.row(slot / GT, [&](auto J) {                              // G27
+        const auto put = [&](auto J) {                               // G27
             if (own) {
                 bk.v[OWN][F_P][J] = mP;
                 bk.v[OWN][F_Q][J] = Qa;
                 bk.v[OWN][F_OID][J] = mOID;
             }
-        });
+        };
+        // the slot's row is at most R: a compare chain instead of the jump table
+        if constexpr (R < KPL) bk.template row_r<R + 1>(slot / GT, put);
+        else bk.row(slot / GT, put);
         if (tid == 0) bk.put_cold(OWN, slot, mTID, mTS, mTNS);  // one writer
         // W = 1: __syncwarp publishes it to the lanes' next cold reads.  W > 1: cold
         // records are read only inside recompute_best_multi, after its first barrier,
