@@ -440,39 +440,39 @@ struct Engine {
     // Eq.5 + G1), then earliest (Ts, Tns), then lowest slot (G4).
     template <int SD>
     __device__ __forceinline__ void recompute_best() {
+        with_rows(hr[SD], [&](auto R) { recompute_best_r<SD, R>(); });
+    }
+    template <int SD, int R>
+    __device__ __forceinline__ void recompute_best_r() {
         if constexpr (W > 1) {
-            recompute_best_multi<SD>();
+            recompute_best_multi<SD, R>();
             return;
         }
         // offset price key (resting prices are >= 1, G22): < 0xffffffff for every
         // occupied slot, so the all-ones minimum means "side empty" (no vote needed)
         unsigned lk = 0xffffffffu;
-        with_rows(hr[SD], [&](auto R) {
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-                const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
-                if (q > 0) lk = min(lk, k);
-            }
-        });
+        for (int j = 0; j < R; ++j) {
+            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+            if (q > 0) lk = min(lk, k);
+        }
         const unsigned m = gmin_u(lk);
         if (m == 0xffffffffu) { bslot[SD] = BEST_EMPTY; return; }
         // candidates at the best price: thread-local earliest (Ts, Tns, row)
         int lts = INT_MAX, ltns = INT_MAX, lj = -1, lc = 0;
         unsigned lv = 0;
-        with_rows(hr[SD], [&](auto R) {
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-                const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
-                if (q > 0 && k == m) {
-                    const int2 t2 = bk.times(SD, j * GT + tid);
-                    if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
-                    ++lc;
-                    lv += (unsigned)q;
-                }
+        for (int j = 0; j < R; ++j) {
+            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+            if (q > 0 && k == m) {
+                const int2 t2 = bk.times(SD, j * GT + tid);
+                if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
+                ++lc;
+                lv += (unsigned)q;
             }
-        });
+        }
         if constexpr (TL1) bV[SD] = gadd(lv);
         const unsigned loc = lj < 0 ? 0xffffffffu : (unsigned)(lj * GT + tid);
         int slot;
@@ -495,33 +495,29 @@ struct Engine {
     // occupied slot and the all-ones value doubles as "side empty".  The time
     // tie-break runs as a warp-level lexicographic (Ts, Tns, slot) minimum whose W
     // winners are exchanged once.
-    template <int SD>
+    template <int SD, int R>
     __device__ __forceinline__ void recompute_best_multi() {
         unsigned lk = 0xffffffffu;
-        with_rows(hr[SD], [&](auto R) {
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-                const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
-                if (q > 0) lk = min(lk, k);
-            }
-        });
+        for (int j = 0; j < R; ++j) {
+            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+            if (q > 0) lk = min(lk, k);
+        }
         const unsigned m = gmin_u(lk);
         if (m == 0xffffffffu) { bslot[SD] = BEST_EMPTY; return; }
         int lts = INT_MAX, ltns = INT_MAX, lj = -1;
         unsigned lv = 0;
-        with_rows(hr[SD], [&](auto R) {
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
-                const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
-                if (q > 0 && k == m) {
-                    const int2 t2 = bk.times(SD, j * GT + tid);
-                    if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
-                    lv += (unsigned)q;
-                }
+        for (int j = 0; j < R; ++j) {
+            const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
+            const unsigned k = (SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p);
+            if (q > 0 && k == m) {
+                const int2 t2 = bk.times(SD, j * GT + tid);
+                if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
+                lv += (unsigned)q;
             }
-        });
+        }
         if constexpr (TL1) bV[SD] = gadd(lv);
         const bool in = lj >= 0;
         const int w1 = __reduce_min_sync(FULL, in ? lts : INT_MAX);
@@ -617,8 +613,26 @@ struct Engine {
         constexpr int OPP = 1 - OWN;
         const int Pa = market ? (OWN == BID ? INT_MAX : 0) : mP;  // P_m = 0 / max_int (G18)
         int Qa = mQ;
+        // the cached best decides most messages without a scan: a side known empty, or
+        // no price overlap with its best order
+        const int bs = bslot[OPP];
+        const bool no_fill = bs == BEST_EMPTY || (bs >= 0 && (OWN == BID ? (Pa < bP[OPP]) : (Pa > bP[OPP])));
+        // the opposite side's row bound is fixed during the fills (they only remove)
+        if (!no_fill && Qa > 0) with_rows(hr[OPP], [&](auto R) { Qa = fill_r<OWN, R>(Pa, Qa, mOID, mTS, mTNS); });
+        if (Qa <= 0) return;
+        if (market) {
+            if (tid == 0) count(ST_DISCARDED, Qa);                   // P:L290
+            return;
+        }
+        // remainder rests as one new order (P:L288) in the lowest empty slot (G3)
+        with_rows(hr[OWN], [&](auto R) { add_r<OWN, R>(Qa, mP, mOID, mTID, mTS, mTNS); });
+    }
+    // the fill loop against the opposite side (rows 0..R-1); returns the remainder Q_a'
+    template <int OWN, int R>
+    __device__ __forceinline__ int fill_r(int Pa, int Qa, int mOID, int mTS, int mTNS) {
+        constexpr int OPP = 1 - OWN;
         while (Qa > 0) {
-            if (bslot[OPP] == BEST_INVALID) recompute_best<OPP>();
+            if (bslot[OPP] == BEST_INVALID) recompute_best_r<OPP, R>();
             const int s = bslot[OPP];
             if (s < 0) break;                                      // side empty
             const int Ps = bP[OPP];
@@ -626,8 +640,8 @@ struct Engine {
             const int ol = s & (GT - 1);
             const bool own = tid == ol;
             const int sj = s / GT;
-            const int myoid = bk.get(OPP, F_OID, sj);              // meaningful on the owner
-            const int Qs = bcast(bk.get(OPP, F_Q, sj), ol);
+            const int myoid = bk.template get_r<R>(OPP, F_OID, sj);  // meaningful on the owner
+            const int Qs = bcast(bk.template get_r<R>(OPP, F_Q, sj), ol);
             const int Qs2 = (Qs - Qa > 0) ? (Qs - Qa) : 0;           // Q_s' = max(0, Q_s - Q_a)
             const int q = Qs - Qs2;                                  // Q_j = Q_s - Q_s'
             Qa = Qa - Qs;                                            // Q_a' = Q_a - Q_s
@@ -641,17 +655,11 @@ struct Engine {
                 part_trd += q;
             }
             ++ntr;                                                   // fills this call (logged = min(ntr, Tcap))
-            bk.put_if(own, OPP, F_Q, sj, Qs2);                       // filled order removed (G10)
+            bk.template put_if_r<R>(own, OPP, F_Q, sj, Qs2);         // filled order removed (G10)
             if constexpr (TL1) bV[OPP] -= (unsigned)q;
             if (Qs2 == 0) bslot[OPP] = BEST_INVALID;
         }
-        if (Qa <= 0) return;
-        if (market) {
-            if (tid == 0) count(ST_DISCARDED, Qa);                   // P:L290
-            return;
-        }
-        // remainder rests as one new order (P:L288) in the lowest empty slot (G3)
-        with_rows(hr[OWN], [&](auto R) { add_r<OWN, R>(Qa, mP, mOID, mTID, mTS, mTNS); });
+        return Qa;
     }
     // the add over the row bound R: free slot in rows 0..R-1, else row R's first slot
     template <int OWN, int R>
