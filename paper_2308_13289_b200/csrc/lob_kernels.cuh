@@ -295,6 +295,7 @@ struct Engine {
     BK bk;
     const Params &p;
     int tid, book, ntr;
+    const unsigned char *scp;  // the same scratch through a shared-memory pointer (uniform loads)
     uint32_t sc;            // shared: counters [NST] int64 (thread 0 only), best times bt[2][2] int32,
                             //         cross-warp exchange xb[2][W] u32, next-book word
     int xph;                // exchange buffer phase (uniform)
@@ -358,7 +359,9 @@ struct Engine {
             const uint32_t base = xbase();
             if (tid == owner) sts32(base, x);
             __syncthreads();
-            const int r = lds32(base);
+            // a plain load from a uniform shared address: the compiler then knows the
+            // value (and the fill loop it controls) is uniform
+            const int r = *reinterpret_cast<const int *>(scp + (8 * NST + 16 + 16 * xph * W));
             xph ^= 1;
             return r;
         }
@@ -990,6 +993,7 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
         e.bk.cold = cold;
         e.bk.tid = tid;
         e.tid = tid; e.book = b; e.ntr = 0; e.sc = scratch; e.xph = 0;
+        e.scp = base + 2 * CH * 32 + 16 + 2 * BK::NP * 16;
         e.part_cxl = 0; e.part_trd = 0;
         e.bk.load(p.book + (size_t)b * 2 * NF * BK::NP);
         e.init_rows();
@@ -1264,6 +1268,7 @@ __global__ void __launch_bounds__(32 * W) lob_export_l2(const int32_t *book, int
     e.bk.tid = threadIdx.x;
     e.bk.cold = smem_u32(dyn);
     e.sc = smem_u32(dyn + 2 * BK::NP * 16);
+    e.scp = dyn + 2 * BK::NP * 16;
     e.bk.load(book + (size_t)b * 2 * NF * BK::NP);
     e.init_rows();
     e.l2_write(out + (size_t)b * L * 4, L);
