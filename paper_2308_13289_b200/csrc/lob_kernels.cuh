@@ -866,12 +866,10 @@ __device__ __forceinline__ void env_agent(E &e, EnvState &es, const Params &p, c
 // lob_reward_kernel), executed quantity, time := the last data message,
 // termination.  The group's first warp; trades were written
 // by their owner threads, hence the barrier.
-template <int W>
-__device__ __forceinline__ void env_post(const Params &p, const EnvParams &ep, int b, int tid, int n, bool have_last,
-                                         int last_ts, int last_tns) {
+// the group's first warp: reward, executed quantity, time, termination
+__device__ __forceinline__ void env_post_warp(const Params &p, const EnvParams &ep, int b, int tid, int n,
+                                              bool have_last, int last_ts, int last_tns) {
     const EnvCfg &c = ep.ec;
-    group_sync<W>();  // also publishes env_agent's state write (thread 0)
-    if (tid >= 32) return;
     EnvState es = ep.env[b];
     const int lane = tid;
     if (es.done) {  // finished before this step (E8)
@@ -880,43 +878,53 @@ __device__ __forceinline__ void env_post(const Params &p, const EnvParams &ep, i
             if (ep.done) ep.done[b] = 1;
             if (ep.executed) ep.executed[b] = es.executed;
         }
-        return;
-    }
-    const int2 *t = reinterpret_cast<const int2 *>(p.trades + (size_t)b * p.Tcap * 6);
-    double sqp = 0.0, sq = 0.0;
-    for (int i = lane; i < n; i += 32) {
-        const int2 pq = t[3 * i];
-        sqp += (double)pq.y * (double)pq.x;
-        sq += (double)pq.y;
-    }
-    sqp = warp_sum(sqp);
-    sq = warp_sum(sq);
-    const double v = sq > 0.0 ? sqp / sq : 0.0;
-    const int lo = c.oid_base, hi = es.next_oid - 1;
-    double adv = 0.0, drift = 0.0;
-    long long qa = 0;
-    for (int i = lane; i < n && sq > 0.0; i += 32) {
-        const int2 pq = t[3 * i], oo = t[3 * i + 1];
-        if ((oo.x >= lo && oo.x <= hi) || (oo.y >= lo && oo.y <= hi)) {
-            adv += (double)pq.y * ((double)pq.x - v);
-            drift += (double)pq.y * (v - es.p_init);
-            qa += pq.y;
+    } else {
+        const int2 *t = reinterpret_cast<const int2 *>(p.trades + (size_t)b * p.Tcap * 6);
+        double sqp = 0.0, sq = 0.0;
+        for (int i = lane; i < n; i += 32) {
+            const int2 pq = t[3 * i];
+            sqp += (double)pq.y * (double)pq.x;
+            sq += (double)pq.y;
+        }
+        sqp = warp_sum(sqp);
+        sq = warp_sum(sq);
+        const double v = sq > 0.0 ? sqp / sq : 0.0;
+        const int lo = c.oid_base, hi = es.next_oid - 1;
+        double adv = 0.0, drift = 0.0;
+        long long qa = 0;
+        for (int i = lane; i < n && sq > 0.0; i += 32) {
+            const int2 pq = t[3 * i], oo = t[3 * i + 1];
+            if ((oo.x >= lo && oo.x <= hi) || (oo.y >= lo && oo.y <= hi)) {
+                adv += (double)pq.y * ((double)pq.x - v);
+                drift += (double)pq.y * (v - es.p_init);
+                qa += pq.y;
+            }
+        }
+        adv = warp_sum(adv);
+        drift = warp_sum(drift);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) qa += __shfl_xor_sync(FULL, qa, o);
+        if (lane == 0) {
+            es.executed += qa;
+            if (have_last) { es.cur_ts = last_ts; es.cur_tns = last_tns; }
+            es.done = (es.executed >= c.task_size) || (env_elapsed_ns(es) > (long long)c.episode_s * 1000000000LL);
+            const double r = adv + c.lam * drift;
+            if (ep.reward) ep.reward[b] = c.task_side == 1 ? -r : r;
+            if (ep.done) ep.done[b] = es.done;
+            if (ep.executed) ep.executed[b] = es.executed;
+            ep.env[b] = es;
         }
     }
-    adv = warp_sum(adv);
-    drift = warp_sum(drift);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) qa += __shfl_xor_sync(FULL, qa, o);
-    if (lane == 0) {
-        es.executed += qa;
-        if (have_last) { es.cur_ts = last_ts; es.cur_tns = last_tns; }
-        es.done = (es.executed >= c.task_size) || (env_elapsed_ns(es) > (long long)c.episode_s * 1000000000LL);
-        const double r = adv + c.lam * drift;
-        if (ep.reward) ep.reward[b] = c.task_side == 1 ? -r : r;
-        if (ep.done) ep.done[b] = es.done;
-        if (ep.executed) ep.executed[b] = es.executed;
-        ep.env[b] = es;
-    }
+}
+
+template <int W>
+__device__ __forceinline__ void env_post(const Params &p, const EnvParams &ep, int b, int tid, int n, bool have_last,
+                                         int last_ts, int last_tns) {
+    group_sync<W>();  // also publishes env_agent's state write (thread 0)
+    // no early returns: a data-dependent exit here made ptxas treat the whole persistent
+    // loop as possibly diverged (reconvergence barriers and divergence checks throughout)
+    if constexpr (W == 1) env_post_warp(p, ep, b, tid, n, have_last, last_ts, last_tns);
+    else if (tid < 32) env_post_warp(p, ep, b, tid, n, have_last, last_ts, last_tns);
 }
 
 // Dynamic shared memory of one CTA of G books of (KPL, W).
