@@ -62,6 +62,16 @@ __device__ __forceinline__ int msg_code(const int4 a) {
     return MC_CANCEL | (S == 1 ? MC_BID : 0) | (cxl ? 0 : MC_AGGR) | (T == 4 ? MC_MKT : 0);
 }
 
+// A message in Eq.6 form made ready for dispatch: the code over T, and a market
+// order's price replaced by the price it matches at (P_m = 0 for a sell, max_int for a
+// buy: P:L290, G18).
+__device__ __forceinline__ int4 msg_decode(int4 a) {
+    const int c = msg_code(a);
+    if ((c & MC_MKT) != 0) a.w = (c & MC_BID) ? INT_MAX : 0;
+    a.x = c;
+    return a;
+}
+
 // NEXT row N3 (execution env, Sec.5.1.3 / 5.2): the task shared by all envs
 // and the per-env state (see lob_env.cuh, include/lob.h lob_env_config)
 struct EnvCfg {  // == lob_env_config (include/lob.h)
@@ -461,7 +471,7 @@ struct Engine {
             if (q > 0) lk = min(lk, k);
         }
         const unsigned m = gmin_u(lk);
-        if (m == 0xffffffffu) { bslot[SD] = BEST_EMPTY; return; }
+        if (m == 0xffffffffu) { set_empty<SD>(); return; }
         // candidates at the best price: thread-local earliest (Ts, Tns, row)
         int lts = INT_MAX, ltns = INT_MAX, lj = -1, lc = 0;
         unsigned lv = 0;
@@ -508,7 +518,7 @@ struct Engine {
             if (q > 0) lk = min(lk, k);
         }
         const unsigned m = gmin_u(lk);
-        if (m == 0xffffffffu) { bslot[SD] = BEST_EMPTY; return; }
+        if (m == 0xffffffffu) { set_empty<SD>(); return; }
         int lts = INT_MAX, ltns = INT_MAX, lj = -1;
         unsigned lv = 0;
 #pragma unroll
@@ -542,6 +552,14 @@ struct Engine {
         set_bt<SD>(b1, b2);
     }
 
+    // an empty side's cached price never overlaps a limit price (1 .. INT_MAX-1 for a
+    // buy against asks, >= 1 for a sell against bids), so the marketability test needs
+    // no separate emptiness check
+    template <int SD>
+    __device__ __forceinline__ void set_empty() {
+        bslot[SD] = BEST_EMPTY;
+        bP[SD] = (SD == ASK) ? INT_MAX : 0;
+    }
     template <int SD>
     __device__ __forceinline__ void set_bt(int ts, int tns) {
         if constexpr (kBtRegs) {
@@ -614,12 +632,11 @@ struct Engine {
     template <int OWN>
     __device__ __forceinline__ void aggress(bool market, int mQ, int mP, int mOID, int mTID, int mTS, int mTNS) {
         constexpr int OPP = 1 - OWN;
-        const int Pa = market ? (OWN == BID ? INT_MAX : 0) : mP;  // P_m = 0 / max_int (G18)
+        const int Pa = mP;  // a market order's P is already 0 / max_int (G18; msg_decode)
         int Qa = mQ;
         // the cached best decides most messages without a scan: a side known empty, or
         // no price overlap with its best order
-        const int bs = bslot[OPP];
-        const bool no_fill = bs == BEST_EMPTY || (bs >= 0 && (OWN == BID ? (Pa < bP[OPP]) : (Pa > bP[OPP])));
+        const bool no_fill = bslot[OPP] != BEST_INVALID && (OWN == BID ? (Pa < bP[OPP]) : (Pa > bP[OPP]));
         // the opposite side's row bound is fixed during the fills (they only remove)
         if (!no_fill && Qa > 0) with_rows(hr[OPP], [&](auto R) { Qa = fill_r<OWN, R>(Pa, Qa, mOID, mTS, mTNS); });
         if (Qa <= 0) return;
@@ -727,9 +744,8 @@ struct Engine {
         }
     }
     // A message in Eq.6 form (the env agent's own orders).
-    __device__ __forceinline__ void message(int4 a, const int4 b) {
-        a.x = msg_code(a);
-        message_coded(a, b);
+    __device__ __forceinline__ void message(const int4 a, const int4 b) {
+        message_coded(msg_decode(a), b);
     }
 
     // L2 (G23): k-th best distinct price per side and its summed quantity;
@@ -1027,7 +1043,9 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
             // decode the chunk lane-parallel: message i's T becomes its dispatch code
             if (tid < cnt) {
                 const uint32_t m = maddr + 32u * (uint32_t)tid;
-                sts32(m, msg_code(lds128(m)));
+                const int4 d = msg_decode(lds128(m));
+                sts32(m, d.x);
+                sts32(m + 12u, d.w);
             }
             group_sync<W>();
             while (cnt > 0) {  // runs up to the next chunk or step end

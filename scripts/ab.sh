@@ -6,7 +6,7 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 cfgs=$1; shift
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/pytest_gpu.log)" > gpurun_out/ab.txt
-for rep in 1 2; do
+for rep in $(seq 1 ${REPS:-2}); do
 for c in $cfgs; do
   for v in "$@"; do
     LOB_LIB_OVERRIDE=variants/$v.so timeout 600 python bench.py --config $c --steps ${STEPS:-10} --e2e-steps 0 --no-cpu-baseline > gpurun_out/ab_${c}_$v.json 2> gpurun_out/ab_${c}_$v.err
