@@ -580,10 +580,6 @@ struct Engine {
         const int bs = bslot[SD];
         if (bs == BEST_INVALID) return;
         bool better = bs == BEST_EMPTY;
-        if constexpr (TL1) {  // level volume: a new level, or one more order at the best price
-            if (better || ((SD == ASK) ? p < bP[SD] : p > bP[SD])) bV[SD] = (unsigned)q;
-            else if (p == bP[SD]) bV[SD] += (unsigned)q;
-        }
         if (!better) {
             const int kn = (SD == ASK) ? p : ~p, kb = (SD == ASK) ? bP[SD] : ~bP[SD];
             better = kn < kb;
@@ -712,6 +708,12 @@ struct Engine {
         // and every such read completes before its second barrier, so the barriers
         // already order this write against earlier and later reads.
         if constexpr (W == 1) group_sync<W>();
+        if constexpr (TL1) {  // level volume: a new best level, or one more order at the best price
+            const int ob = bslot[OWN], op = bP[OWN];
+            const bool lvl = ob == BEST_EMPTY || (ob >= 0 && ((OWN == ASK) ? mP < op : mP > op));
+            const bool same = ob >= 0 && mP == op;
+            bV[OWN] = lvl ? (unsigned)Qa : (same ? bV[OWN] + (unsigned)Qa : bV[OWN]);
+        }
         note_add<OWN>(slot, mP, mTS, mTNS, Qa);
     }
 
