@@ -2,8 +2,8 @@
 //
 // A GROUP of W warps (GT = 32*W threads) owns one book (PAPER.md P:L320:
 // messages within a book are strictly serial; books are independent).  W = 1
-// for capacity N <= 256 (one warp per book, several books per CTA); for larger
-// books W = N/256 warps of one CTA share the book.  Slot i of a side (Eq.1,
+// for capacity N <= 512 (one warp per book, several books per CTA); larger books
+// have W = 4 warps of one CTA (8 or 16 rows each; lob_api.cu geo_of).  Slot i of a side (Eq.1,
 // P:L161-163) lives in thread (i % GT), row (i / GT) -- "interleaved" -- so:
 //   * every lowest-index search (free slot P:L175/G3, order-id lookup P:L177,
 //     lowest-slot tie-break G4) is a thread-local select over rows plus ONE
@@ -226,7 +226,15 @@ struct RegBook {
                 case 4: if constexpr (KPL_ > 4) f(IC<(KPL_ > 4 ? 4 : 0)>{}); break;
                 case 5: if constexpr (KPL_ > 5) f(IC<(KPL_ > 5 ? 5 : 0)>{}); break;
                 case 6: if constexpr (KPL_ > 6) f(IC<(KPL_ > 6 ? 6 : 0)>{}); break;
-                default: if constexpr (KPL_ > 7) f(IC<(KPL_ > 7 ? 7 : 0)>{}); break;
+                case 7: if constexpr (KPL_ > 7) f(IC<(KPL_ > 7 ? 7 : 0)>{}); break;
+            case 8: if constexpr (KPL_ > 8) f(IC<(KPL_ > 8 ? 8 : 0)>{}); break;
+            case 9: if constexpr (KPL_ > 9) f(IC<(KPL_ > 9 ? 9 : 0)>{}); break;
+            case 10: if constexpr (KPL_ > 10) f(IC<(KPL_ > 10 ? 10 : 0)>{}); break;
+            case 11: if constexpr (KPL_ > 11) f(IC<(KPL_ > 11 ? 11 : 0)>{}); break;
+            case 12: if constexpr (KPL_ > 12) f(IC<(KPL_ > 12 ? 12 : 0)>{}); break;
+            case 13: if constexpr (KPL_ > 13) f(IC<(KPL_ > 13 ? 13 : 0)>{}); break;
+            case 14: if constexpr (KPL_ > 14) f(IC<(KPL_ > 14 ? 14 : 0)>{}); break;
+            default: if constexpr (KPL_ > 15) f(IC<(KPL_ > 15 ? 15 : 0)>{}); break;
             }
         }
     }
@@ -406,9 +414,13 @@ struct Engine {
         } else if constexpr (KPL <= 4) {
             if (h < 2) f(IC<2>{});
             else f(IC<KPL>{});
-        } else {
+        } else if constexpr (KPL <= 8) {
             if (h < 2) f(IC<2>{});
             else if (h < 4) f(IC<4>{});
+            else f(IC<KPL>{});
+        } else {
+            if (h < 4) f(IC<4>{});
+            else if (h < 8) f(IC<8>{});
             else f(IC<KPL>{});
         }
     }
@@ -961,7 +973,7 @@ constexpr int step_smem_bytes() {
 // MODE 3 = MODE 0 built for 8 CTAs/SM (64 registers) instead of 7: more spills, more
 // warps; chosen by the host for many-wave batches of 4-row books (C4: +1.7 %)
 template <int KPL, int W, int G, int MODE>
-__global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : 16 / W)))))
+__global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : (KPL > 8 ? 12 / W : 16 / W))))))
     lob_step(const Params p, const EnvParams ep) {
     using BK = RegBook<KPL, W>;
     constexpr bool TL1 = MODE == 1, ENV = MODE == 2;
