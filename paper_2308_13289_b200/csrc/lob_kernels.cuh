@@ -255,11 +255,6 @@ struct RegBook {
         for (int jj = 1; jj < KPL_; ++jj) r = (j == jj) ? v[s][f][jj] : r;
         return r;
     }
-    __device__ __forceinline__ void put_if(bool pred, int s, int f, int j, int32_t x) {
-#pragma unroll
-        for (int jj = 0; jj < KPL_; ++jj)
-            if (pred && j == jj) v[s][f][jj] = x;
-    }
     // the same for a row known to be below R (shorter select chains)
     template <int R>
     __device__ __forceinline__ int32_t get_r(int s, int f, int j) const {
@@ -365,10 +360,6 @@ struct Engine {
         if constexpr (W == 1) return r;
         else return __reduce_add_sync(FULL, exchange(r, 0u));
     }
-    __device__ __forceinline__ bool gany(bool b) {
-        if constexpr (W == 1) return __any_sync(FULL, b);
-        else return __any_sync(FULL, exchange(__any_sync(FULL, b) ? 1u : 0u, 0u) != 0u);
-    }
     // value held by thread `owner` of the group, to every thread
     __device__ __forceinline__ int bcast(int x, int owner) {
         if constexpr (W == 1) {
@@ -385,18 +376,6 @@ struct Engine {
         }
     }
 
-    // Lowest slot whose thread-local predicate holds, or a value >= NP (none): one
-    // group minimum of (row*GT + tid), which is exactly the slot index (interleaved
-    // layout).  The select chain picks a constant row (KPL = none), so the slot is
-    // formed once with one multiply-add instead of one add per row.
-    template <class Pred>
-    __device__ __forceinline__ int lowest(Pred pred) {
-        unsigned r = KPL;
-#pragma unroll
-        for (int j = KPL - 1; j >= 0; --j)
-            if (pred(j)) r = (unsigned)j;
-        return (int)gmin_u(r * GT + (unsigned)tid);
-    }
     static __device__ __forceinline__ bool found(int slot) { return (unsigned)slot < (unsigned)BK::NP; }
 
     // Row high-water mark: every occupied slot of side s lies in rows 0..hr[s] (-1: no
@@ -441,24 +420,16 @@ struct Engine {
             hr[ASK] = hr[BID] = KPL - 1;
         }
     }
-    // lowest slot of rows 0..R-1 whose predicate holds, or >= NP
+    // Lowest slot of rows 0..R-1 whose thread-local predicate holds, or a value >= NP
+    // (none, see found): the select chain picks a constant row (KPL = none), then ONE
+    // group minimum of (row*GT + tid), which is exactly the slot index (interleaved
+    // layout) -- one multiply-add instead of one add per row.
     template <int R, class Pred>
     __device__ __forceinline__ int lowest_rows(Pred pred) {
         unsigned r = KPL;
 #pragma unroll
         for (int j = R - 1; j >= 0; --j)
             if (pred(j)) r = (unsigned)j;
-        return (int)gmin_u(r * GT + (unsigned)tid);
-    }
-    // lowest occupied slot (pred includes Q > 0) on side SD, or >= NP
-    template <int SD, class Pred>
-    __device__ __forceinline__ int lowest_occ(Pred pred) {
-        unsigned r = KPL;
-        with_rows(hr[SD], [&](auto R) {
-#pragma unroll
-            for (int j = R - 1; j >= 0; --j)
-                if (pred(j)) r = (unsigned)j;
-        });
         return (int)gmin_u(r * GT + (unsigned)tid);
     }
     // Best(o_s) of side SD over occupied slots: price (ask min / bid max,
