@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4")
+    ap.add_argument("--books", type=int, default=0,
+                    help="override the config's books per GPU (the K sweep of SURVEY.md 8(d))")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -222,6 +224,8 @@ def main():
         else:
             dist.init_process_group(backend)
     cfg = lobgen.CONFIGS[args.config]
+    if args.books > 0:
+        cfg = cfg.with_(n_books=args.books)
     book0, K = shard_books(rank, world, cfg.n_books, args.scaling)
     cfg = cfg.with_(n_books=K)
     S, M, L = cfg.n_steps, cfg.msgs_per_step, cfg.l2_levels
