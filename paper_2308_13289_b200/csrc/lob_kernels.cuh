@@ -199,7 +199,8 @@ __device__ __forceinline__ void group_sync() {
 
 // ---------------------------------------------------------------- book storage
 // Hot fields P, Q, OID of slot (j*GT + tid) in registers v[s][f][j]; cold
-// fields in shared memory, one 16-byte record per slot: {Ts, Tns, TID, 0}.
+// fields in shared memory, one 16-byte record per slot: {OID, TID, Ts, Tns}
+// (the message quad as loaded; its OID word is not read).
 template <int KPL_, int W_>
 struct RegBook {
     static constexpr int KPL = KPL_, W = W_, GT = 32 * W_, NP = KPL_ * 32 * W_;
@@ -208,9 +209,12 @@ struct RegBook {
     int tid;        // thread index within the book group
     __device__ __forceinline__ int32_t hot(int s, int f, int j) const { return v[s][f][j]; }
     __device__ __forceinline__ uint32_t rec(int s, int slot) const { return cold + 16u * (uint32_t)(s * NP + slot); }
-    __device__ __forceinline__ int2 times(int s, int slot) const { return lds64x2(rec(s, slot)); }
+    // record = the message's second quad in Eq.6 order {OID, TID, Ts, Tns}: an add stores
+    // it as loaded, without reordering moves (the OID word is unused here)
+    __device__ __forceinline__ int2 times(int s, int slot) const { return lds64x2(rec(s, slot) + 8u); }
+    __device__ __forceinline__ void put_cold(int s, int slot, const int4 b) const { sts128(rec(s, slot), b); }
     __device__ __forceinline__ void put_cold(int s, int slot, int tid_, int ts, int tns) const {
-        sts128(rec(s, slot), make_int4(ts, tns, tid_, 0));
+        sts128(rec(s, slot), make_int4(0, tid_, ts, tns));
     }
     // run f(row) with the uniform row as a compile-time constant
     template <class F>
@@ -294,9 +298,9 @@ struct RegBook {
 #pragma unroll
                 for (int f = 0; f < 3; ++f) __stcs(r + f * NP, occ ? v[s][f][j] : -1);
                 const int4 c = lds128(rec(s, j * GT + tid));
-                __stcs(r + F_TID * NP, occ ? c.z : -1);
-                __stcs(r + F_TS * NP, occ ? c.x : -1);
-                __stcs(r + F_TNS * NP, occ ? c.y : -1);
+                __stcs(r + F_TID * NP, occ ? c.y : -1);
+                __stcs(r + F_TS * NP, occ ? c.z : -1);
+                __stcs(r + F_TNS * NP, occ ? c.w : -1);
             }
     }
 };
@@ -685,7 +689,7 @@ struct Engine {
         // the slot's row is at most R: a compare chain instead of the jump table
         if constexpr (R < KPL) bk.template row_r<R + 1>(slot / GT, put);
         else bk.row(slot / GT, put);
-        if (tid == 0) bk.put_cold(OWN, slot, mTID, mTS, mTNS);  // one writer
+        if (tid == 0) bk.put_cold(OWN, slot, make_int4(mOID, mTID, mTS, mTNS));  // one writer
         // W = 1: __syncwarp publishes it to the lanes' next cold reads.  W > 1: cold
         // records are read only inside recompute_best_multi, after its first barrier,
         // and every such read completes before its second barrier, so the barriers
