@@ -319,7 +319,7 @@ struct Engine {
     // uniform best-order cache per side (Eq.5 + G1/G4): slot or BEST_*, and its price
     int bslot[2], bP[2];
     // best order's (Ts, Tns): uniform registers for multi-warp books (no barriers),
-    // shared memory for warp books (saves 4 registers on the 72-register kernel)
+    // shared memory for warp books (4 registers fewer in the 64-register kernel)
     static constexpr bool kBtRegs = (W > 1);
     int bTS[2], bTNS[2];
     int hr[2];              // row high-water mark per side (see with_rows)
@@ -945,8 +945,9 @@ constexpr int step_smem_bytes() {
 // dynamic counter.  MODE 0 (and 3): L2 per step; MODE 1 also writes the Level-1
 // trace (NEXT N1); MODE 2 is one fused execution-env step (NEXT N3, env_agent /
 // env_post).
-// MODE 3 = MODE 0 built for 8 CTAs/SM (64 registers) instead of 7: more spills, more
-// warps; chosen by the host for many-wave batches of 4-row books (C4: +1.7 %)
+// MODE 3 = MODE 0 built for 8 CTAs/SM (64 registers); chosen by the host for many-wave
+// batches of 4-row books.  (With the uniform persistent loop MODE 0 also fits in 64
+// registers without spills, so the two now compile alike; MODE 3 keeps the hard cap.)
 template <int KPL, int W, int G, int MODE>
 __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : (KPL > 8 ? 12 / W : 16 / W))))))
     lob_step(const Params p, const EnvParams ep) {
