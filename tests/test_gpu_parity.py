@@ -474,3 +474,56 @@ def test_env_episode_in_cuda_graph():
         assert np.all(np.abs(rew[s].cpu().numpy() - ro) <= 1e-12 * np.maximum(1.0, scale)), s
     np.testing.assert_array_equal(b.book().cpu().numpy(), oe.book())
     np.testing.assert_array_equal(b.stats().cpu().numpy(), oe.stats())
+
+
+def _edge_stream(rng, n):
+    """Messages at the value boundaries the kernel special-cases: empty sides, market
+    orders (P rewritten to 0 / max_int at decode), limits at P = max_int (the empty-ask
+    sentinel), Q = max_int, OIDs at -9000 / INT_MIN / INT_MAX, malformed codes."""
+    IMAX, IMIN = 2**31 - 1, -2**31
+    out = np.zeros((n, 8), np.int32)
+    for i in range(n):
+        k = rng.integers(0, 12)
+        S = int(rng.choice([-1, 1]))
+        ts, tns = 34200 + i // 7, int(rng.integers(0, 10**9))
+        oid = int(rng.choice([i + 1, i + 1, i + 1, -9000, -9001, IMIN, IMAX, int(rng.integers(1, 40))]))
+        if k == 0:
+            out[i] = (4, S, int(rng.choice([1, 50, IMAX])), int(rng.integers(-5, 5)), oid, 7, ts, tns)  # market
+        elif k == 1:
+            out[i] = (1, S, int(rng.integers(1, 300)), IMAX, oid, 7, ts, tns)                           # limit at max_int
+        elif k == 2:
+            out[i] = (1, S, int(rng.choice([1, IMAX])), int(rng.choice([1, 2, IMAX - 1])), oid, 7, ts, tns)
+        elif k in (3, 4):
+            out[i] = (int(rng.choice([2, 3])), S, int(rng.choice([1, 10, IMAX])), int(rng.choice([1, IMAX, 100])),
+                      int(rng.integers(1, i + 2)) if k == 3 else oid, 7, ts, tns)                         # cancels
+        elif k == 5:
+            out[i] = (int(rng.integers(-2, 7)), int(rng.integers(-2, 3)), int(rng.integers(-3, 3)),
+                      int(rng.integers(-3, 3)), oid, 7, ts, tns)                                           # malformed / padding
+        else:
+            out[i] = (1, S, int(rng.integers(1, 500)), 1000 + int(rng.integers(-8, 8)) * 10, oid, 7, ts, tns)
+    return out
+
+
+@pytest.mark.parametrize("wide,N,l1", [(False, 100, False), (True, 100, False), (False, 100, True), (False, 7, False),
+                                       (True, 128, False), (False, 300, False), (False, 1500, False)])
+def test_edge_values_and_empty_sides(monkeypatch, wide, N, l1):
+    if wide:
+        monkeypatch.setenv("LOB_FORCE_WIDE", "1")
+    K, S, M = 64, 6, 25
+    rng = np.random.default_rng(N + 7 * wide + 3 * l1)
+    msgs = np.stack([_edge_stream(rng, S * M) for _ in range(K)])
+    g, o = GpuEngine(K, N, 40, 6), oracle.OracleBatch(K, N, 40, 6)
+    res = []
+    for e in (g, o):
+        e.init(None, 0, 0)
+        out = e.process(msgs, S, M, l2=True, l1=l1)
+        tr, cnt = e.trades()
+        res.append((out, e.book(), tr, cnt, e.stats(), e.l2()))
+    for a, b, what in zip(res[0], res[1], ("out", "book", "trades", "n_trades", "stats", "l2_now")):
+        if what == "out" and l1:
+            np.testing.assert_array_equal(a[0], b[0], err_msg="l2")
+            np.testing.assert_array_equal(a[1], b[1], err_msg="l1")
+        else:
+            np.testing.assert_array_equal(a, b, err_msg=what)
+    assert res[0][4][:, STAT_NAMES.index("market_discarded_qty")].sum() > 0
+    assert res[0][4][:, STAT_NAMES.index("bad")].sum() > 0
