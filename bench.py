@@ -304,7 +304,9 @@ def main():
                 "traffic": None, "kernel": "lobk::lob_step<4,1,4,3> (lob_process_messages; MODE 3 = the 8-CTA/SM build for many-wave batches)",
                 "kernel_ms": kmean_ms, "kernel_share_of_step": kmean_ms / ms_per_step,
                 "alg_bytes_per_launch": alg_bytes, "alg_bytes_per_msg": alg_bytes / (K * cfg.n_msgs),
-                "peak_source": peak_src}
+                "peak_source": peak_src,
+                "note": "HBM fraction as BASELINE.json asks; the kernel is instruction-bound -- the binding "
+                        "ceilings are roofline_alu_pipe and roofline_issue (DESIGN.md section 8)"}
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     roofline_issue = None
     roofline_alu_pipe = None
