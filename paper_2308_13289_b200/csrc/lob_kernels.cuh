@@ -967,8 +967,10 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
     // the group index through a warp reduction: ptxas then knows it (and every shared
     // address below) is warp-uniform, so messages loaded from those addresses are
     // uniform and the dispatch branches need no reconvergence (BSSY/BSYNC) and the
-    // warp collectives no divergence check (BRA.DIV)
-    const int g = G == 1 ? 0 : (int)__reduce_min_sync(FULL, threadIdx.x / (32 * W));
+    // warp collectives no divergence check (BRA.DIV).  Kept even when G = 1 (the
+    // value is then 0): a one-warp build without this opening collective compiled
+    // with 66 divergence checks.
+    const int g = (int)__reduce_min_sync(FULL, threadIdx.x / (32 * W));
     const int tid = (int)opaque(threadIdx.x % (32 * W));
     // carve this group's region: stage [2][CH][32 B] | bars [2] | cold [2][NP][16 B] | scratch
     unsigned char *base = dyn + g * (step_smem_bytes<KPL, W, G>() / G);
