@@ -188,6 +188,37 @@ __device__ __forceinline__ void sts128(uint32_t a, int4 v) {
                  : "memory");
 }
 
+// Single-writer stores as predicated instructions inside one asm block (all lanes
+// execute it, only lane `who == 0` / the lane whose `pred` holds writes): no
+// lane-divergent branch in the message loop, so ptxas proves the whole message body
+// uniform and dispatches it on the uniform datapath (R2UR + ULOP3 + BRA.U).  Used by
+// the many-wave build (MODE 3: C4 +1.6 %); the other builds measured slower with it.
+__device__ __forceinline__ void sts32_if0(int who, uint32_t a, int v) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %0, 0;\n\t@p st.shared.b32 [%1], %2;\n\t}" ::"r"(who), "r"(a),
+                 "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void sts128_if0(int who, uint32_t a, int4 v) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %0, 0;\n\t@p st.shared.v4.b32 [%1], {%2, %3, %4, %5};\n\t}" ::"r"(who),
+                 "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void add64_if0(int who, uint32_t a, long long x) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 v;\n\tsetp.eq.s32 p, %0, 0;\n\t@p ld.shared.b64 v, [%1];\n\t"
+        "@p add.s64 v, v, %2;\n\t@p st.shared.b64 [%1], v;\n\t}" ::"r"(who),
+        "r"(a), "l"(x)
+        : "memory");
+}
+// the Eq.3 trade record (24 bytes) by the lane whose `pred` holds
+__device__ __forceinline__ void trade_store_if(bool pred, int2 *t, int2 a, int2 b, int2 c) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.v2.b32 [%1], {%2, %3};\n\t"
+        "@p st.global.v2.b32 [%1+8], {%4, %5};\n\t@p st.global.v2.b32 [%1+16], {%6, %7};\n\t}" ::"r"((unsigned)pred),
+        "l"(t), "r"(a.x), "r"(a.y), "r"(b.x), "r"(b.y), "r"(c.x), "r"(c.y)
+        : "memory");
+}
+
 // ------------------------------------------------------------ group primitives
 // Barrier over the book's threads: the warp itself, or the whole CTA (W > 1
 // books own their CTA).
@@ -306,7 +337,7 @@ struct RegBook {
 };
 
 // ------------------------------------------------------------------ the engine
-template <class BK, bool TL1 = false, bool ROWS = false>
+template <class BK, bool TL1 = false, bool ROWS = false, bool PRED = false>
 struct Engine {
     static constexpr int KPL = BK::KPL, W = BK::W, GT = BK::GT;
     BK bk;
@@ -553,7 +584,10 @@ struct Engine {
             bTS[SD] = ts; bTNS[SD] = tns;
         } else {
             group_sync<W>();                 // earlier readers of bt are done
-            if (tid == 0) {                  // one writer, published to the group
+            if constexpr (PRED) {            // one writer, published to the group
+                sts32_if0(tid, bt_addr(SD, 0), ts);
+                sts32_if0(tid, bt_addr(SD, 1), tns);
+            } else if (tid == 0) {
                 sts32(bt_addr(SD, 0), ts);
                 sts32(bt_addr(SD, 1), tns);
             }
@@ -597,7 +631,11 @@ struct Engine {
             slot = lowest_rows<R>([&](int j) {
                 return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
             });
-        if (!found(slot)) { if (tid == 0) count(ST_UNKNOWN, 1); return; }  // G15
+        if (!found(slot)) {                        // G15
+            if constexpr (PRED) add64_if0(tid, sc + 8u * ST_UNKNOWN, 1);
+            else if (tid == 0) count(ST_UNKNOWN, 1);
+            return;
+        }
         const bool own = tid == (slot & (GT - 1));
         const int j = slot / GT;                   // the slot is occupied: its row is below R
         const int qi = bk.template get_r<R>(SD, F_Q, j);
@@ -648,8 +686,13 @@ struct Engine {
             const int Qs2 = (Qs - Qa > 0) ? (Qs - Qa) : 0;           // Q_s' = max(0, Q_s - Q_a)
             const int q = Qs - Qs2;                                  // Q_j = Q_s - Q_s'
             Qa = Qa - Qs;                                            // Q_a' = Q_a - Q_s
-            if (own) {
-                if (ntr < p.Tcap) {                                  // Eq.3 record, Eq.4 cap (G8)
+            if constexpr (PRED) {                                    // Eq.3 record, Eq.4 cap (G8)
+                trade_store_if(own && ntr < p.Tcap,
+                               reinterpret_cast<int2 *>(p.trades + ((size_t)book * p.Tcap + ntr) * 6),
+                               make_int2(Ps, q), make_int2(mOID, myoid), make_int2(mTS, mTNS));
+                if (own) part_trd += q;
+            } else if (own) {
+                if (ntr < p.Tcap) {
                     int2 *t = reinterpret_cast<int2 *>(p.trades + ((size_t)book * p.Tcap + ntr) * 6);
                     t[0] = make_int2(Ps, q);
                     t[1] = make_int2(mOID, myoid);
@@ -689,7 +732,8 @@ struct Engine {
         // the slot's row is at most R: a compare chain instead of the jump table
         if constexpr (R < KPL) bk.template row_r<R + 1>(slot / GT, put);
         else bk.row(slot / GT, put);
-        if (tid == 0) bk.put_cold(OWN, slot, make_int4(mOID, mTID, mTS, mTNS));  // one writer
+        if constexpr (PRED) sts128_if0(tid, bk.rec(OWN, slot), make_int4(mOID, mTID, mTS, mTNS));  // one writer
+        else if (tid == 0) bk.put_cold(OWN, slot, make_int4(mOID, mTID, mTS, mTNS));
         // W = 1: __syncwarp publishes it to the lanes' next cold reads.  W > 1: cold
         // records are read only inside recompute_best_multi, after its first barrier,
         // and every such read completes before its second barrier, so the barriers
@@ -1011,7 +1055,7 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
             }
         }
         if (tid < NST) sts64(scratch + 8u * tid, 0);
-        Engine<BK, TL1, kRows> e(p);
+        Engine<BK, TL1, kRows, MODE == 3> e(p);
         e.bk.cold = cold;
         e.bk.tid = tid;
         e.tid = tid; e.book = b; e.ntr = 0; e.sc = scratch; e.xph = 0;
