@@ -337,7 +337,7 @@ struct RegBook {
 };
 
 // ------------------------------------------------------------------ the engine
-template <class BK, bool TL1 = false, bool ROWS = false, bool PRED = false>
+template <class BK, bool TL1 = false, bool ROWS = false, bool PRED = false, bool PREDT = PRED>
 struct Engine {
     static constexpr int KPL = BK::KPL, W = BK::W, GT = BK::GT;
     BK bk;
@@ -686,7 +686,7 @@ struct Engine {
             const int Qs2 = (Qs - Qa > 0) ? (Qs - Qa) : 0;           // Q_s' = max(0, Q_s - Q_a)
             const int q = Qs - Qs2;                                  // Q_j = Q_s - Q_s'
             Qa = Qa - Qs;                                            // Q_a' = Q_a - Q_s
-            if constexpr (PRED) {                                    // Eq.3 record, Eq.4 cap (G8)
+            if constexpr (PREDT) {                                   // Eq.3 record, Eq.4 cap (G8)
                 trade_store_if(own && ntr < p.Tcap,
                                reinterpret_cast<int2 *>(p.trades + ((size_t)book * p.Tcap + ntr) * 6),
                                make_int2(Ps, q), make_int2(mOID, myoid), make_int2(mTS, mTNS));
@@ -1055,7 +1055,7 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
             }
         }
         if (tid < NST) sts64(scratch + 8u * tid, 0);
-        Engine<BK, TL1, kRows, MODE == 3> e(p);
+        Engine<BK, TL1, kRows, MODE == 3, MODE == 3 || (MODE == 0 && KPL <= 4)> e(p);
         e.bk.cold = cold;
         e.bk.tid = tid;
         e.tid = tid; e.book = b; e.ntr = 0; e.sc = scratch; e.xph = 0;
