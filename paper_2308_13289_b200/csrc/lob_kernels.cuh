@@ -1055,7 +1055,10 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
             }
         }
         if (tid < NST) sts64(scratch + 8u * tid, 0);
-        Engine<BK, TL1, kRows, MODE == 3, MODE == 3 || (MODE == 0 && KPL <= 4)> e(p);
+        // predicated single-writer stores (sts32_if0 ...): all of them in the many-wave
+        // build, the trade record in every one-warp build up to 8 rows (C2 +3 %, C3 +2 %,
+        // env step -7 %; measured slower for the 16-row build and the other stores)
+        Engine<BK, TL1, kRows, MODE == 3, MODE == 3 || (W == 1 && KPL <= 8)> e(p);
         e.bk.cold = cold;
         e.bk.tid = tid;
         e.tid = tid; e.book = b; e.ntr = 0; e.sc = scratch; e.xph = 0;
