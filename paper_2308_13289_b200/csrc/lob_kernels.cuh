@@ -210,6 +210,12 @@ __device__ __forceinline__ void add64_if0(int who, uint32_t a, long long x) {
         "r"(a), "l"(x)
         : "memory");
 }
+// a 16-byte global record by lane `who == 0`
+__device__ __forceinline__ void stg128_if0(int who, int32_t *g, int4 v) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %0, 0;\n\t@p st.global.v4.b32 [%1], {%2, %3, %4, %5};\n\t}" ::"r"(who),
+                 "l"(g), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
 // the Eq.3 trade record (24 bytes) by the lane whose `pred` holds
 __device__ __forceinline__ void trade_store_if(bool pred, int2 *t, int2 a, int2 b, int2 c) {
     asm volatile(
@@ -753,11 +759,9 @@ struct Engine {
     __device__ __forceinline__ void l1_write(int32_t *dst) {
         if (bslot[ASK] == BEST_INVALID) recompute_best<ASK>();
         if (bslot[BID] == BEST_INVALID) recompute_best<BID>();
-        if (tid == 0) {
-            const bool a = bslot[ASK] >= 0, b = bslot[BID] >= 0;
-            *reinterpret_cast<int4 *>(dst) = make_int4(a ? bP[ASK] : -1, a ? (int)bV[ASK] : 0, b ? bP[BID] : -1,
-                                                       b ? (int)bV[BID] : 0);
-        }
+        const bool a = bslot[ASK] >= 0, b = bslot[BID] >= 0;
+        // predicated store (no lane-divergent branch in the message loop)
+        stg128_if0(tid, dst, make_int4(a ? bP[ASK] : -1, a ? (int)bV[ASK] : 0, b ? bP[BID] : -1, b ? (int)bV[BID] : 0));
     }
 
     // A message whose first word holds its dispatch code (msg_code) instead of T.
