@@ -105,3 +105,23 @@ def test_step_kernels_are_warp_uniform():
         n_div = f.count("BRA.DIV")
         assert n_div == 0, f"lob_step<KPL={m.group(1)}, W=1, MODE={m.group(2)}> has {n_div} BRA.DIV"
     assert checked >= 19, checked  # MODE 0 (step), 1 (L1 trace), 2 (fused env step), 3 (many-wave step)
+
+
+def test_bench_kernel_register_budget():
+    """Performance guard: the C4 bench kernel (lob_step<4,1,4,3>, 8 CTAs/SM) must fit in
+    64 registers without spills ("Occupancy").  Reads the ptxas
+    report `make` writes next to the library; skipped when the library was built
+    elsewhere."""
+    log = os.path.join(PKG, "ptxas.log")
+    if not os.path.exists(log):
+        pytest.skip("no ptxas.log (library not built here)")
+    lines = open(log).read().splitlines()
+    for i, line in enumerate(lines):
+        if "Compiling entry function '_ZN4lobk8lob_stepILi4ELi1ELi4ELi3E" in line:
+            block = "\n".join(lines[i:i + 6])
+            m = re.search(r"Used (\d+) registers", block)
+            s = re.search(r"(\d+) bytes spill stores", block)
+            assert m and int(m.group(1)) <= 64, block
+            assert s and int(s.group(1)) == 0, block
+            return
+    pytest.skip("bench kernel not in ptxas.log")
