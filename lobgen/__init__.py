@@ -22,7 +22,7 @@ _lock = threading.Lock()
 _lib = None
 
 PROFILES = {"lobster": 0, "heavy_market": 1, "cancel_heavy": 2, "ties": 3, "overflow": 4,
-            "synthetic": 5, "garbage": 6}
+            "synthetic": 5, "garbage": 6, "saturate": 7}
 INIT_TS, INIT_TNS = 34200, 0          # 09:30:00 in LOBSTER seconds-after-midnight
 TICK, REF0 = 100, 1_000_000
 

@@ -26,7 +26,7 @@
 #define LOT 100
 
 enum { P_LOBSTER = 0, P_HEAVY_MARKET = 1, P_CANCEL_HEAVY = 2, P_TIES = 3, P_OVERFLOW = 4,
-       P_SYNTHETIC = 5, P_GARBAGE = 6, P_NPROFILES = 7 };
+       P_SYNTHETIC = 5, P_GARBAGE = 6, P_SATURATE = 7, P_NPROFILES = 8 };
 
 typedef struct {
     int limit, cancel, del, market;  /* mix, percent (sums to 100) */
@@ -47,6 +47,7 @@ static const profile_t PROFILES[P_NPROFILES] = {
     /* overflow     */ {70,  5, 20,  5, 10,  5, 0,  0, 0, 0,  0},
     /* synthetic    */ {40, 25, 30,  5, 10,  5, 0,  0, 0, 1, 50},
     /* garbage      */ {50, 10, 35,  5, 10,  5, 0,  0, 5, 1,  0},
+    /* saturate     */ {95,  3,  2,  0,  0,  5, 0,  0, 0, 0,  0},  /* passive limits fill both sides past N */
 };
 
 /* ---------------------------------------------------------------- RNG */

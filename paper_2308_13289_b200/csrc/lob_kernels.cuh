@@ -369,7 +369,6 @@ struct Engine {
     __device__ __forceinline__ void count(int c, long long x) {  // thread 0 only
         sts64(sc + 8u * c, lds64(sc + 8u * c) + x);
     }
-    __device__ __forceinline__ bool valid(int j) const { return j < KPL - 1 || j * GT + tid < p.N; }
     __device__ __forceinline__ uint32_t bt_addr(int sd, int k) const { return sc + 8u * NST + 4u * (2 * sd + k); }
 
     // ---- group reductions: warp REDUX, then (W > 1) one exchange through shared memory
@@ -713,16 +712,20 @@ struct Engine {
         }
         return Qa;
     }
-    // the add over the row bound R: free slot in rows 0..R-1, else row R's first slot
+    // the add over the row bound R: free slot in rows 0..R-1, else row R's first slot.
+    // Capacity (G6): the geometry pads N to NP >= N slots, and the padding slots are
+    // empty (-1), so the group minimum may land on one; slot indices grow with the row,
+    // so the minimum over all empty slots is below N exactly when a free slot < N
+    // exists -- ONE compare against N after the reduction decides saturation.
     template <int OWN, int R>
     __device__ __forceinline__ void add_r(int Qa, int mP, int mOID, int mTID, int mTS, int mTNS) {
         unsigned r = KPL;
-        if constexpr (R < KPL) r = valid(R) ? (unsigned)R : (unsigned)KPL;
+        if constexpr (R < KPL) r = (unsigned)R;
 #pragma unroll
         for (int j = R - 1; j >= 0; --j)
-            if (valid(j) && bk.hot(OWN, F_Q, j) <= 0) r = (unsigned)j;
+            if (bk.hot(OWN, F_Q, j) <= 0) r = (unsigned)j;
         const int slot = (int)gmin_u(r * GT + (unsigned)tid);
-        if (!found(slot)) {                                          // side saturated (G6)
+        if (slot >= p.N) {                                           // side saturated (G6)
             if (tid == 0) { count(ST_ADD_OVF, 1); count(ST_OVF_QTY, Qa); }
             return;
         }

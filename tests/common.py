@@ -126,3 +126,16 @@ def assert_outputs_equal(a, b, books=None, what=""):
         if not np.array_equal(x, y):
             bad = np.argwhere(x != y)
             raise AssertionError(f"{what}: {key} differs at {len(bad)} positions, first {bad[:5].tolist()}")
+
+
+# Capacity contract (G6) in every padded geometry: the kernel pads N to NP = 32*W*KPL
+# slots (N = 130 -> 256, 600 -> 1024, 1500 -> 2048); a saturating stream (passive limits
+# on both sides, about 5N messages) drives every capacity band past N.
+SATURATE_N = [16, 100, 130, 224, 250, 300, 480, 600, 896, 1025, 1500, 1920]
+
+
+def saturate_cfg(N):
+    import lobgen
+    K = 48 if N <= 300 else (16 if N <= 1024 else 8)
+    steps = -(-(5 * N) // 100)
+    return lobgen.Config("sat", K, N, steps, 100, min(N // 4, 30), 64, 10, "saturate", 100 + N)

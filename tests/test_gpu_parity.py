@@ -9,7 +9,8 @@ import torch
 
 import lobgen
 import oracle
-from common import STAT_NAMES, assert_outputs_equal, golden_cases, run_engine, run_golden_case
+from common import (SATURATE_N, STAT_NAMES, assert_outputs_equal, golden_cases, run_engine, run_golden_case,
+                    saturate_cfg)
 
 pytestmark = pytest.mark.gpu
 
@@ -527,3 +528,22 @@ def test_edge_values_and_empty_sides(monkeypatch, wide, N, l1):
             np.testing.assert_array_equal(a, b, err_msg=what)
     assert res[0][4][:, STAT_NAMES.index("market_discarded_qty")].sum() > 0
     assert res[0][4][:, STAT_NAMES.index("bad")].sum() > 0
+
+
+# ------------------------------------- capacity contract (G6) in every padded geometry
+# geo_of pads N to NP = 32*W*KPL slots (e.g. N = 130 -> 256); the padding slots are
+# empty and must never take an order (common.saturate_cfg: more passive limits than N).
+@pytest.mark.parametrize("N", SATURATE_N)
+@pytest.mark.parametrize("wide", [False, True])
+def test_capacity_saturated(monkeypatch, N, wide):
+    if wide and N > 128:
+        pytest.skip("the many-wave build exists for 4-row books only")
+    if wide:
+        monkeypatch.setenv("LOB_FORCE_WIDE", "1")
+    cfg = saturate_cfg(N)
+    g, o = _both(cfg, calls=2 if cfg.n_steps % 2 == 0 else 1)
+    assert_outputs_equal(g, o, what=f"saturate N={N}")
+    ov = o["stats"][:, STAT_NAMES.index("add_overflow")]
+    assert (ov > 0).mean() >= 0.5, "the stream must overflow most books"
+    occ = (o["book"][..., 1] > 0).sum(-1)
+    assert (occ <= N).all() and (occ.max() == N)

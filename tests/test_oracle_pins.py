@@ -266,3 +266,20 @@ def test_l1_trace_equals_fifo_top_of_book(profile):
         np.testing.assert_array_equal(l1[k], np.asarray(snaps, np.int32)[:, 0], err_msg=f"book {k}")
         # consistency with the per-step L2 (level 1 at the step boundaries)
         np.testing.assert_array_equal(l1[k, cfg.msgs_per_step - 1::cfg.msgs_per_step], l2[k, :, 0])
+
+
+def test_saturate_profile_reaches_capacity():
+    """The GPU capacity test (test_gpu_parity.py::test_capacity_saturated) is only
+    meaningful if its streams saturate: on the oracle most books overflow (G6), some
+    side ends exactly full, and no side ever holds more than N orders."""
+    from common import SATURATE_N, saturate_cfg
+    for N in SATURATE_N:
+        cfg = saturate_cfg(N)
+        msgs, init = lobgen.generate(cfg)
+        o = oracle.OracleBatch(cfg.n_books, N, cfg.trades_cap, cfg.l2_levels, threads=8)
+        o.init(init, lobgen.INIT_TS, lobgen.INIT_TNS)
+        o.process(msgs, cfg.n_steps, cfg.msgs_per_step)
+        st = o.stats()
+        assert (st[:, STAT_NAMES.index("add_overflow")] > 0).mean() >= 0.5, N
+        occ = (o.book()[..., 1] > 0).sum(-1)
+        assert occ.max() == N and (occ <= N).all(), N
