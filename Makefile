@@ -10,11 +10,13 @@ PKG       := paper_2308_13289_b200
 LIB       := $(PKG)/liblob.so
 SRCS      := $(PKG)/csrc/lob_api.cu
 DEPS      := $(SRCS) $(PKG)/csrc/lob_kernels.cuh $(PKG)/csrc/lob_env.cuh include/lob.h
+# provenance: hash of the engine sources + this Makefile (flags), exported by lob_build_id()
+BUILD_ID  := $(shell cat $(DEPS) Makefile | sha256sum | cut -c1-16)
 
 all: $(LIB) $(PKG)/liblobster.so oracle/liblob_oracle.so lobgen/liblobgen.so
 
-$(LIB): $(DEPS)
-	$(NVCC) $(NVFLAGS) -o $@.tmp $(SRCS) 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; exit 1)
+$(LIB): $(DEPS) Makefile
+	$(NVCC) $(NVFLAGS) -DLOB_BUILD_ID='"$(BUILD_ID)"' -o $@.tmp $(SRCS) 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; exit 1)
 	mv $@.tmp $@
 	@grep -E "Compiling entry|registers|spill" $(PKG)/ptxas.log | grep -B1 -E "spill stores [1-9]|bytes spill" || true
 

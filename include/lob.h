@@ -119,16 +119,28 @@ int lob_process_messages(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps,
 int lob_process_messages_l1(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t msgs_per_step,
                             int32_t *d_l2_out, int32_t *d_l1_out, void *cuda_stream);
 
-/* Same call with HOST buffers (end-to-end path): copies h_msgs (pinned host,
- * [K][n_steps*msgs_per_step][8]) into the caller's device buffer d_msgs_buf,
- * processes it, and copies the L2 snapshots (if h_l2_out is non-NULL; device
- * staging in d_l2_buf, [K][n_steps][L][4]) and the counters (if h_stats_out is
- * non-NULL, [K][LOB_NSTATS] int64, staged in the state) back to the host.
- * Books are processed in `chunks` slices so that copies overlap kernels; all
- * work is enqueued on cuda_stream plus one internal event chain, and the
- * caller synchronises the stream before reading host outputs. */
+/* Same call with HOST buffers (the end-to-end path: every output of the method comes
+ * back to the host).  Copies h_msgs (pinned host, [K][n_steps*msgs_per_step][8]) into
+ * the caller's device buffer d_msgs_buf, processes it, and returns to the host:
+ *  h_l2_out          NULL or [K][n_steps][L][4] int32 L2 snapshots (device staging in
+ *                    d_l2_buf, same shape);
+ *  h_stats_out       NULL or [K][LOB_NSTATS] int64 counters;
+ *  h_trades_out      NULL or pinned (page-locked, mapped) host memory of capacity
+ *                    K*trades_cap rows of [6] int32: the call's LOGGED trade rows
+ *                    (Eq.3), book 0's first, then book 1's, ... packed
+ *                    without gaps (book k's rows start at sum of counts[0..k-1]); rows
+ *                    past the total are not written.  Written by a device kernel
+ *                    straight into the host buffer, so only logged rows cross PCIe;
+ *  h_trade_counts_out  [K] int32 logged rows per book (required with h_trades_out).
+ * Books are processed in `chunks` slices so that copies overlap kernels.  All work is
+ * enqueued on cuda_stream and two copy streams the context owns (created on first use,
+ * joined back to cuda_stream by events), so the call may be captured into a CUDA graph
+ * from cuda_stream.  The caller synchronises the stream before reading host outputs.
+ * Errors: LOB_EINVAL for null required buffers, misaligned device buffers (16 B) or
+ * trade output (8 B), or an h_trades_out that is not pinned mapped memory. */
 int lob_process_messages_host(lob_ctx *ctx, const int32_t *h_msgs, int32_t n_steps,
                               int32_t msgs_per_step, int32_t *h_l2_out, int64_t *h_stats_out,
+                              int32_t *h_trades_out, int32_t *h_trade_counts_out,
                               int32_t *d_msgs_buf, int32_t *d_l2_buf, int32_t chunks,
                               void *cuda_stream);
 
@@ -160,7 +172,7 @@ typedef struct {
     int32_t episode_s;      /* episode length in seconds; forced market order
                                for the remaining task 60 s before the end      */
     int32_t agent_tid;      /* TID stamped on the agent's orders                        */
-    int32_t agent_oid_base; /* the agent's OIDs are base, base+1, ... (G29)            */
+    int32_t agent_oid_base; /* the agent's OIDs are base, base+1, ... (G29); > 0       */
     int32_t reserved;
     double lambda;          /* drift weight of eq:rewardfunc               */
 } lob_env_config;
@@ -169,7 +181,9 @@ typedef struct {
 size_t lob_env_state_bytes(int32_t n_envs);
 
 /* After lob_init: start an episode in every book: P_init = (best ask + best bid)/2
- * of the current book, time = (init_ts, init_tns), executed = 0. */
+ * of the current book, time = (init_ts, init_tns), executed = 0.
+ * lob_env_reset and lob_env_step return LOB_EINVAL for an invalid cfg (task_side not
+ * +-1, task_size/tick/episode_s <= 0, n_passive < 0, agent_oid_base <= 0). */
 int lob_env_reset(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, int32_t init_ts,
                   int32_t init_tns, void *cuda_stream);
 
@@ -213,6 +227,10 @@ int lob_digest(lob_ctx *ctx, uint64_t *d_out, void *cuda_stream);
 
 /* Number of kernels this process has launched through the library (all contexts). */
 int64_t lob_launch_count(void);
+
+/* Build provenance: a hash of the sources and build flags the library was compiled
+ * from (Makefile LOB_BUILD_ID), so measurements can be tied to the binary that made them. */
+const char *lob_build_id(void);
 
 const char *lob_strerror(int code);
 const char *lob_last_error(void); /* thread-local detail for the last failure */

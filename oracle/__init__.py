@@ -40,35 +40,48 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
-def _load():
+_variants = {}
+
+
+def _declare(lib):
+    P = ctypes.c_void_p
+    i32 = ctypes.c_int32
+    lib.oracle_create.restype = P
+    lib.oracle_create.argtypes = [i32, i32, i32, i32, i32]
+    lib.oracle_destroy.argtypes = [P]
+    lib.oracle_init.restype = ctypes.c_int
+    lib.oracle_init.argtypes = [P, i32, i32, P, i32, i32, i32]
+    lib.oracle_process.restype = ctypes.c_int
+    lib.oracle_process.argtypes = [P, i32, i32, P, i32, i32, P]
+    lib.oracle_process_ex.restype = ctypes.c_int
+    lib.oracle_process_ex.argtypes = [P, i32, i32, P, i32, i32, P, P]
+    for name in ("oracle_get_book", "oracle_get_l2", "oracle_get_stats",
+                 "oracle_get_violations"):
+        getattr(lib, name).argtypes = [P, P]
+    lib.oracle_get_trades.argtypes = [P, P, P]
+    lib.oracle_step_reward.argtypes = [P, P, P, P, ctypes.c_double, P, P, P]
+    lib.oracle_env_create.restype = P
+    lib.oracle_env_create.argtypes = [i32]
+    lib.oracle_env_destroy.argtypes = [P]
+    lib.oracle_env_reset.argtypes = [P, P, P, i32, i32]
+    lib.oracle_env_step.argtypes = [P, P, P, P, P, i32, P, P, P, P]
+    lib.oracle_env_get.argtypes = [P, P, P]
+    return lib
+
+
+def _load(path: str | None = None):
+    """The oracle library; `path` loads a separately compiled variant of lob_oracle.c
+    (tests/test_oracle_mutations.py compiles deliberately broken copies to show that
+    the pins catch them)."""
     global _lib
     with _lock:
+        if path is not None:
+            if path not in _variants:
+                _variants[path] = _declare(ctypes.CDLL(path))
+            return _variants[path]
         if _lib is None:
             build()
-            lib = ctypes.CDLL(_LIB)
-            P = ctypes.c_void_p
-            i32 = ctypes.c_int32
-            lib.oracle_create.restype = P
-            lib.oracle_create.argtypes = [i32, i32, i32, i32, i32]
-            lib.oracle_destroy.argtypes = [P]
-            lib.oracle_init.restype = ctypes.c_int
-            lib.oracle_init.argtypes = [P, i32, i32, P, i32, i32, i32]
-            lib.oracle_process.restype = ctypes.c_int
-            lib.oracle_process.argtypes = [P, i32, i32, P, i32, i32, P]
-            lib.oracle_process_ex.restype = ctypes.c_int
-            lib.oracle_process_ex.argtypes = [P, i32, i32, P, i32, i32, P, P]
-            for name in ("oracle_get_book", "oracle_get_l2", "oracle_get_stats",
-                         "oracle_get_violations"):
-                getattr(lib, name).argtypes = [P, P]
-            lib.oracle_get_trades.argtypes = [P, P, P]
-            lib.oracle_step_reward.argtypes = [P, P, P, P, ctypes.c_double, P, P, P]
-            lib.oracle_env_create.restype = P
-            lib.oracle_env_create.argtypes = [i32]
-            lib.oracle_env_destroy.argtypes = [P]
-            lib.oracle_env_reset.argtypes = [P, P, P, i32, i32]
-            lib.oracle_env_step.argtypes = [P, P, P, P, P, i32, P, P, P, P]
-            lib.oracle_env_get.argtypes = [P, P, P]
-            _lib = lib
+            _lib = _declare(ctypes.CDLL(_LIB))
     return _lib
 
 
@@ -80,8 +93,8 @@ class OracleBatch:
     """K independent books of capacity N (SURVEY 8(c) pseudo-code, in C)."""
 
     def __init__(self, n_books: int, capacity: int, trades_cap: int | None = None,
-                 l2_levels: int = 10, check: bool = False, threads: int = 1):
-        self.lib = _load()
+                 l2_levels: int = 10, check: bool = False, threads: int = 1, lib_path: str | None = None):
+        self.lib = _load(lib_path)
         self.K, self.N = int(n_books), int(capacity)
         self.T_cap = self.N if trades_cap is None else int(trades_cap)
         self.L = int(l2_levels)

@@ -79,6 +79,7 @@ typedef struct {
     /* bookkeeping used only by the invariant checker (check mode) */
     int64_t limit_in, limit_aggr_traded, limit_rested, market_in, market_aggr_traded;
     int64_t resting_init;
+    int64_t call_trades0, call_dropped0;   /* counters at the start of the current call */
     int64_t violations;
 } obook;
 
@@ -157,6 +158,10 @@ static void check_book(oracle_ctx *X, obook *b) {
     if (b->limit_in != b->limit_aggr_traded + b->limit_rested + b->c[C_OVERFLOW_QTY]) b->violations++;
     /* market qty in = traded as aggressor + discarded */
     if (b->market_in != b->market_aggr_traded + b->c[C_MARKET_DISCARDED_QTY]) b->violations++;
+    /* every fill of this call is logged or counted as dropped (Eq.4, G8) */
+    if (b->c[C_TRADES] - b->call_trades0 != b->n_trades + (b->c[C_TRADES_DROPPED] - b->call_dropped0))
+        b->violations++;
+    if (b->n_trades > X->T_cap) b->violations++;
 }
 
 /* Priority check: no occupied slot on the standing side has a strictly
@@ -371,6 +376,7 @@ static void init_book(oracle_ctx *X, obook *b, const int32_t *l2 /*[L0][4] or NU
     for (int i = 0; i < X->T_cap; i++) for (int f = 0; f < T_NF; f++) b->trades[(size_t)i * T_NF + f] = -1;
     b->n_trades = 0;
     memset(b->c, 0, sizeof(b->c));
+    b->call_trades0 = b->call_dropped0 = 0;
     b->limit_in = b->limit_aggr_traded = b->limit_rested = b->market_in = b->market_aggr_traded = 0;
     b->violations = 0;
     int32_t oid = -9000;
@@ -410,6 +416,8 @@ int oracle_process_ex(oracle_ctx *X, int32_t k0, int32_t k1, const int32_t *msgs
         obook *b = &X->books[k];
         for (int i = 0; i < X->T_cap; i++) for (int f = 0; f < T_NF; f++) b->trades[(size_t)i * T_NF + f] = -1;
         b->n_trades = 0;
+        b->call_trades0 = b->c[C_TRADES];
+        b->call_dropped0 = b->c[C_TRADES_DROPPED];
         const int32_t *mk = msgs + (size_t)k * per_book * M_NF;
         for (int s = 0; s < n_steps; s++) {
             for (int i = 0; i < M; i++) {
@@ -623,6 +631,8 @@ void oracle_env_step(oracle_ctx *X, void *envp, const env_cfg *c, const float *a
         /* one call of 8 + M messages: the trade log is the step's (G9) */
         for (int i = 0; i < X->T_cap; i++) for (int f = 0; f < T_NF; f++) b->trades[(size_t)i * T_NF + f] = -1;
         b->n_trades = 0;
+        b->call_trades0 = b->c[C_TRADES];
+        b->call_dropped0 = b->c[C_TRADES_DROPPED];
         for (int i = 0; i < 8 + M; i++) process(X, b, stream + (size_t)i * M_NF);
         if (was_done) { reward[k] = 0.0; done[k] = 1; executed[k] = e->executed; continue; }
         int32_t agent[2] = {c->oid_base, e->next_oid - 1};

@@ -55,7 +55,7 @@ Geo geo_of(int N) {
 
 struct Layout {
     int NP;
-    size_t off_book, off_trades, off_ntr, off_stats, off_sched, total;
+    size_t off_book, off_trades, off_ntr, off_stats, off_sched, off_tro, total;
 };
 
 bool layout_of(const lob_config *c, Layout *L) {
@@ -71,7 +71,9 @@ bool layout_of(const lob_config *c, Layout *L) {
     L->off_ntr = al(L->off_trades + K * (size_t)c->trades_cap * 6 * sizeof(int32_t));
     L->off_stats = al(L->off_ntr + K * sizeof(int32_t));
     L->off_sched = al(L->off_stats + K * NST * sizeof(long long));
-    L->total = al(L->off_sched + 2 * sizeof(unsigned));
+    // host path only: per-book row offsets of the packed trade copy + the running total
+    L->off_tro = al(L->off_sched + 2 * sizeof(unsigned));
+    L->total = al(L->off_tro + (K + 1) * sizeof(long long));
     return true;
 }
 }  // namespace
@@ -86,11 +88,16 @@ struct lob_ctx {
     bool force_wide;  // test hook (env LOB_FORCE_WIDE=1): MODE 3 for every 4-row batch
     int grid_limit;   // test hook (env LOB_GRID_CAP=n): at most n CTAs per step launch, so
                       // small batches exercise the dynamic book scheduler
+    // lob_process_messages_host: copy streams and fork/join events, created on first use
+    // and kept for the context's lifetime (none per call)
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_h = nullptr, ev_k = nullptr;
     int32_t *book() const { return reinterpret_cast<int32_t *>(state + lay.off_book); }
     int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
     int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
     long long *stats() const { return reinterpret_cast<long long *>(state + lay.off_stats); }
     unsigned *sched() const { return reinterpret_cast<unsigned *>(state + lay.off_sched); }
+    long long *tro() const { return reinterpret_cast<long long *>(state + lay.off_tro); }
 };
 
 namespace {
@@ -232,7 +239,14 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
     return LOB_OK;
 }
 
-void lob_destroy(lob_ctx *ctx) { delete ctx; }
+void lob_destroy(lob_ctx *ctx) {
+    if (!ctx) return;
+    if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+    if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
+    for (cudaEvent_t e : {ctx->ev_start, ctx->ev_h, ctx->ev_k})
+        if (e) cudaEventDestroy(e);
+    delete ctx;
+}
 
 int lob_init(lob_ctx *ctx, const int32_t *d_init_l2, int32_t init_levels, int32_t init_ts, int32_t init_tns,
              void *stream) {
@@ -282,8 +296,9 @@ int lob_process_messages_l1(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps
 }
 
 int lob_process_messages_host(lob_ctx *ctx, const int32_t *h_msgs, int32_t n_steps, int32_t msgs_per_step,
-                              int32_t *h_l2_out, int64_t *h_stats_out, int32_t *d_msgs_buf, int32_t *d_l2_buf,
-                              int32_t chunks, void *stream) {
+                              int32_t *h_l2_out, int64_t *h_stats_out, int32_t *h_trades_out,
+                              int32_t *h_trade_counts_out, int32_t *d_msgs_buf, int32_t *d_l2_buf, int32_t chunks,
+                              void *stream) {
     int rc = check_ctx(ctx);
     if (rc) return rc;
     if (n_steps < 0 || msgs_per_step < 0 || chunks < 1) return fail(LOB_EINVAL, "bad n_steps/msgs_per_step/chunks%s");
@@ -293,61 +308,96 @@ int lob_process_messages_host(lob_ctx *ctx, const int32_t *h_msgs, int32_t n_ste
     if (K == 0) return LOB_OK;
     if ((nmsg > 0 && (!h_msgs || !d_msgs_buf)) || (h_l2_out && !d_l2_buf))
         return fail(LOB_EINVAL, "null buffer%s");
+    if (h_trades_out && !h_trade_counts_out) return fail(LOB_EINVAL, "h_trades_out needs h_trade_counts_out%s");
+    if (reinterpret_cast<uintptr_t>(d_msgs_buf) % 16 || reinterpret_cast<uintptr_t>(d_l2_buf) % 16 ||
+        reinterpret_cast<uintptr_t>(h_trades_out) % 8)
+        return fail(LOB_EINVAL, "misaligned buffer%s");
+    // the packed trade rows are written by a kernel straight into the caller's pinned
+    // host buffer (mapped through unified addressing): only logged rows cross PCIe
+    int2 *trades_dst = nullptr;
+    if (h_trades_out && ctx->cfg.trades_cap > 0) {
+        void *dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, h_trades_out, 0) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(LOB_EINVAL, "h_trades_out must be pinned (page-locked, mapped) host memory%s");
+        }
+        trades_dst = static_cast<int2 *>(dp);
+    }
     if (msgs_per_step == 0) n_steps = 0;
     cudaStream_t st = (cudaStream_t)stream;
-    const int L = ctx->cfg.l2_levels;
+    cudaError_t e = cudaSuccess;
+    if (!ctx->h2d) {  // first use: the context's copy streams and events
+        e = cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_h, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_k, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "copy stream / event creation");
+    }
+    cudaStream_t h2d = ctx->h2d, d2h = ctx->d2h;
+    const int L = ctx->cfg.l2_levels, Tcap = ctx->cfg.trades_cap;
     const size_t msg_bytes_pb = (size_t)nmsg * 8 * sizeof(int32_t);
     const size_t l2_bytes_pb = (size_t)n_steps * L * 4 * sizeof(int32_t);
     const int per = (K + chunks - 1) / chunks;
-    // Three-stage pipeline over book chunks: H2D(i) on `h2d`, kernel(i) on the
-    // caller's stream after H2D(i), D2H(i) on `d2h` after kernel(i); copies of
-    // neighbouring chunks overlap the kernels on the two copy engines.
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaError_t e = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
-    cudaEvent_t start, done_h, done_k;
-    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&done_h, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&done_k, cudaEventDisableTiming);
-    cudaEventRecord(start, st);
-    cudaStreamWaitEvent(h2d, start, 0);
-    cudaStreamWaitEvent(d2h, start, 0);
+    // checked enqueue: the first failing CUDA call sets rc (later calls are skipped)
+    auto ck = [&](cudaError_t r, const char *what) {
+        if (rc == LOB_OK && r != cudaSuccess) rc = cuda_fail(r, what);
+        return rc == LOB_OK;
+    };
+    // Three-stage pipeline over book chunks: H2D(i) on `h2d`, kernel(i) on the caller's
+    // stream after H2D(i), then on `d2h` after kernel(i): the L2 copy and the trade
+    // packing of chunk i.  Copies of neighbouring chunks overlap the kernels on the two
+    // copy engines.  Fork/join through events only, so the whole call can be captured
+    // into a CUDA graph from the caller's stream.
+    ck(cudaEventRecord(ctx->ev_start, st), "event record");
+    ck(cudaStreamWaitEvent(h2d, ctx->ev_start, 0), "stream wait");
+    ck(cudaStreamWaitEvent(d2h, ctx->ev_start, 0), "stream wait");
+    if (trades_dst) ck(cudaMemsetAsync(ctx->tro() + K, 0, sizeof(long long), d2h), "memset");
     for (int i = 0; i < chunks && rc == LOB_OK; ++i) {
         const int b0 = i * per, nb = (b0 + per <= K) ? per : K - b0;
         if (nb <= 0) break;
-        if (msg_bytes_pb) {
-            e = cudaMemcpyAsync((char *)d_msgs_buf + (size_t)b0 * msg_bytes_pb,
-                                (const char *)h_msgs + (size_t)b0 * msg_bytes_pb, (size_t)nb * msg_bytes_pb,
-                                cudaMemcpyHostToDevice, h2d);
-            if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
-        }
-        cudaEventRecord(done_h, h2d);          // events may be re-recorded: waits capture the
-        cudaStreamWaitEvent(st, done_h, 0);    // state at the time of the wait call
+        if (msg_bytes_pb)
+            ck(cudaMemcpyAsync((char *)d_msgs_buf + (size_t)b0 * msg_bytes_pb,
+                               (const char *)h_msgs + (size_t)b0 * msg_bytes_pb, (size_t)nb * msg_bytes_pb,
+                               cudaMemcpyHostToDevice, h2d), "H2D messages");
+        ck(cudaEventRecord(ctx->ev_h, h2d), "event record");  // a wait captures the event's
+        ck(cudaStreamWaitEvent(st, ctx->ev_h, 0), "stream wait");  // state at the wait call
+        if (rc) break;
         rc = launch_step(ctx, d_msgs_buf + (size_t)b0 * nmsg * 8, n_steps, msgs_per_step,
                          (h_l2_out && n_steps) ? d_l2_buf + (size_t)b0 * n_steps * L * 4 : nullptr, b0, nb, st);
         if (rc) break;
-        if (h_l2_out && l2_bytes_pb) {
-            cudaEventRecord(done_k, st);
-            cudaStreamWaitEvent(d2h, done_k, 0);
-            e = cudaMemcpyAsync((char *)h_l2_out + (size_t)b0 * l2_bytes_pb,
-                                (char *)d_l2_buf + (size_t)b0 * l2_bytes_pb, (size_t)nb * l2_bytes_pb,
-                                cudaMemcpyDeviceToHost, d2h);
-            if (e != cudaSuccess) { rc = cuda_fail(e, "D2H"); break; }
+        const bool l2c = h_l2_out && l2_bytes_pb;
+        if (l2c || trades_dst) {
+            ck(cudaEventRecord(ctx->ev_k, st), "event record");
+            ck(cudaStreamWaitEvent(d2h, ctx->ev_k, 0), "stream wait");
+        }
+        if (l2c)
+            ck(cudaMemcpyAsync((char *)h_l2_out + (size_t)b0 * l2_bytes_pb, (char *)d_l2_buf + (size_t)b0 * l2_bytes_pb,
+                               (size_t)nb * l2_bytes_pb, cudaMemcpyDeviceToHost, d2h), "D2H L2");
+        if (trades_dst && rc == LOB_OK) {
+            // row offsets of this chunk's books after every earlier chunk's rows, then the
+            // logged rows of each book to host row offs[b] (books in order: packed)
+            lob_trade_offsets<<<1, 1024, 0, d2h>>>(ctx->ntr(), ctx->tro(), b0, nb, K);
+            rc = after_launch("lob_trade_offsets");
+            if (rc == LOB_OK) {
+                lob_pack_trades<<<blocks_for((long long)nb * 32, 256), 256, 0, d2h>>>(ctx->trades(), ctx->ntr(),
+                                                                                      ctx->tro(), b0, nb, Tcap,
+                                                                                      trades_dst);
+                rc = after_launch("lob_pack_trades");
+            }
         }
     }
-    cudaEventRecord(done_h, d2h);              // the caller's stream completes after every D2H
-    cudaStreamWaitEvent(st, done_h, 0);
-    if (rc == LOB_OK && h_stats_out) {
-        e = cudaMemcpyAsync(h_stats_out, ctx->stats(), (size_t)K * NST * sizeof(long long), cudaMemcpyDeviceToHost, st);
-        if (e != cudaSuccess) rc = cuda_fail(e, "D2H stats");
-    }
-    // resources are released once the enqueued work no longer needs them
-    cudaEventDestroy(start);
-    cudaEventDestroy(done_h);
-    cudaEventDestroy(done_k);
-    cudaStreamDestroy(h2d);
-    cudaStreamDestroy(d2h);
+    // join: the caller's stream continues after every D2H (also on failure, so the
+    // context's streams never run ahead of the caller's)
+    cudaError_t j1 = cudaEventRecord(ctx->ev_h, d2h);
+    cudaError_t j2 = j1 == cudaSuccess ? cudaStreamWaitEvent(st, ctx->ev_h, 0) : j1;
+    ck(j2, "join");
+    if (rc == LOB_OK && h_stats_out)
+        ck(cudaMemcpyAsync(h_stats_out, ctx->stats(), (size_t)K * NST * sizeof(long long), cudaMemcpyDeviceToHost, st),
+           "D2H stats");
+    if (rc == LOB_OK && h_trade_counts_out)
+        ck(cudaMemcpyAsync(h_trade_counts_out, ctx->ntr(), (size_t)K * sizeof(int32_t), cudaMemcpyDeviceToHost, st),
+           "D2H trade counts");
     return rc;
 }
 
@@ -370,9 +420,11 @@ int lob_step_reward(lob_ctx *ctx, const int32_t *d_agent_oids, const double *d_p
 
 size_t lob_env_state_bytes(int32_t n_envs) { return n_envs < 0 ? 0 : (size_t)n_envs * sizeof(EnvState); }
 
+// agent_oid_base > 0: a live agent order is remembered by its OID with 0 meaning "none"
+// (EnvState::live), so the agent's OIDs base, base+1, ... must never include 0 (E4)
 static int env_cfg_ok(const lob_env_config *c) {
     return c && (c->task_side == 1 || c->task_side == -1) && c->task_size > 0 && c->tick > 0 && c->n_passive >= 0 &&
-           c->episode_s > 0;
+           c->episode_s > 0 && c->agent_oid_base > 0;
 }
 
 int lob_env_reset(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, int32_t init_ts, int32_t init_tns,
@@ -480,6 +532,11 @@ int lob_digest(lob_ctx *ctx, uint64_t *d_out, void *stream) {
 }
 
 int64_t lob_launch_count(void) { return g_launches.load(); }
+
+#ifndef LOB_BUILD_ID
+#define LOB_BUILD_ID "unknown"
+#endif
+const char *lob_build_id(void) { return LOB_BUILD_ID; }
 
 const char *lob_strerror(int code) {
     switch (code) {

@@ -1296,6 +1296,56 @@ __global__ void lob_export_trades(const int32_t *trades, const int32_t *ntrades,
     if (counts && t < K) counts[t] = ntrades[t];
 }
 
+// Host path (lob_process_messages_host): packed copy of the logged trade rows.
+// Row offsets of books [b0, b0+nb): an exclusive scan of the logged-row counts,
+// continuing the running total tro[K] of the earlier chunks (one CTA of 1024 threads).
+__global__ void __launch_bounds__(1024) lob_trade_offsets(const int32_t *ntrades, long long *tro, int b0, int nb,
+                                                          int K) {
+    __shared__ long long wsum[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    long long base = tro[K];
+    for (int i0 = 0; i0 < nb; i0 += 1024) {
+        const int i = i0 + t;
+        const long long c = i < nb ? ntrades[b0 + i] : 0;
+        long long x = c;  // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            long long v = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(FULL, v, o);
+                if (lane >= o) v += y;
+            }
+            wsum[lane] = v;  // inclusive over warps
+        }
+        __syncthreads();
+        const long long before = (w > 0 ? wsum[w - 1] : 0) + x - c;
+        if (i < nb) tro[b0 + i] = base + before;
+        base += wsum[31];
+        __syncthreads();
+    }
+    if (t == 0) tro[K] = base;
+}
+// One warp per book: its logged rows (24 B each, contiguous) to row tro[b] of `dst`
+// (8-byte words, coalesced; `dst` may be mapped pinned host memory).
+__global__ void lob_pack_trades(const int32_t *trades, const int32_t *ntrades, const long long *tro, int b0, int nb,
+                                int Tcap, int2 *dst) {
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= nb) return;
+    const int b = b0 + (int)gw;
+    const int n = ntrades[b] * 3;  // int2 words
+    const int2 *src = reinterpret_cast<const int2 *>(trades + (size_t)b * Tcap * 6);
+    int2 *d = dst + tro[b] * 3;
+    for (int i = lane; i < n; i += 32) d[i] = src[i];
+}
+
 // per-book FNV-1a-64 over the exported state (include/lob.h lob_digest): one thread per book
 __device__ __forceinline__ unsigned long long fnv1a_word(unsigned long long h, uint32_t w) {
 #pragma unroll

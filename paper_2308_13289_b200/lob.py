@@ -66,7 +66,8 @@ def lib():
                 L.lob_process_messages_l1.restype = ctypes.c_int
                 L.lob_process_messages_l1.argtypes = [P, P, i32, i32, P, P, P]
             L.lob_process_messages_host.restype = ctypes.c_int
-            L.lob_process_messages_host.argtypes = [P, P, i32, i32, P, P, P, P, i32, P]
+            L.lob_process_messages_host.argtypes = [P, P, i32, i32, P, P, P, P, P, P, i32, P]
+            L.lob_build_id.restype = ctypes.c_char_p
             for name in ("lob_get_l2", "lob_get_book", "lob_get_stats"):
                 getattr(L, name).restype = ctypes.c_int
                 getattr(L, name).argtypes = [P, P, P]
@@ -103,6 +104,11 @@ def launch_count() -> int:
     return int(lib().lob_launch_count())
 
 
+def build_id() -> str:
+    """Hash of the sources and flags liblob.so was built from (lob_build_id)."""
+    return lib().lob_build_id().decode()
+
+
 def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
@@ -110,6 +116,28 @@ def _ptr(t):
 def _stream(stream=None):
     s = torch.cuda.current_stream() if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
+
+
+class _On:
+    """Run a call's conversions, allocations and launch on ONE stream: ``stream=`` if
+    given (made current for the block, so torch's copies and allocations are ordered
+    with the kernel), else torch's current stream of the batch's device."""
+
+    def __init__(self, device, stream):
+        self.device, self.stream = device, stream
+
+    def __enter__(self):
+        self._d = torch.cuda.device(self.device)
+        self._d.__enter__()
+        self._s = torch.cuda.stream(self.stream) if self.stream is not None else None
+        if self._s is not None:
+            self._s.__enter__()
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def __exit__(self, *a):
+        if self._s is not None:
+            self._s.__exit__(*a)
+        self._d.__exit__(*a)
 
 
 class LobBatch:
@@ -161,13 +189,12 @@ class LobBatch:
     # ------------------------------------------------------------------ calls
     def init(self, init_l2=None, init_ts: int = 0, init_tns: int = 0, stream=None):
         """lob_init: empty books, optional synthetic L2 seed [K][L0][4]."""
-        t = self._dev(init_l2)
-        L0 = 0 if t is None else int(t.shape[1])
-        if t is not None:
-            assert t.shape == (self.K, L0, 4), t.shape
-        with torch.cuda.device(self.device):
-            _check(lib().lob_init(self.ctx, _ptr(t), L0, int(init_ts), int(init_tns), _stream(stream)),
-                   "lob_init")
+        with _On(self.device, stream) as st:
+            t = self._dev(init_l2)
+            L0 = 0 if t is None else int(t.shape[1])
+            if t is not None:
+                assert t.shape == (self.K, L0, 4), t.shape
+            _check(lib().lob_init(self.ctx, _ptr(t), L0, int(init_ts), int(init_tns), st), "lob_init")
         self._keep = t  # keep the input alive until the stream has consumed it
 
     def process(self, msgs, n_steps: int, msgs_per_step: int, l2: bool = True, l2_out=None,
@@ -176,22 +203,22 @@ class LobBatch:
 
         With ``l1=True`` (lob_process_messages_l1, NEXT row N1) returns ``(l2, l1)`` where
         l1 [K][n_steps*msgs_per_step][4] is the Level-1 state after every message."""
-        m = self._dev(msgs)
-        assert m.shape == (self.K, n_steps * msgs_per_step, 8), m.shape
-        out = l2_out
-        if l2 and out is None:
-            out = torch.empty((self.K, n_steps, self.L, 4), dtype=torch.int32, device=self.device)
-        l1o = l1_out
-        if l1 and l1o is None:
-            l1o = torch.empty((self.K, n_steps * msgs_per_step, 4), dtype=torch.int32, device=self.device)
-        with torch.cuda.device(self.device):
+        with _On(self.device, stream) as st:
+            m = self._dev(msgs)
+            assert m.shape == (self.K, n_steps * msgs_per_step, 8), m.shape
+            out = l2_out
+            if l2 and out is None:
+                out = torch.empty((self.K, n_steps, self.L, 4), dtype=torch.int32, device=self.device)
+            l1o = l1_out
+            if l1 and l1o is None:
+                l1o = torch.empty((self.K, n_steps * msgs_per_step, 4), dtype=torch.int32, device=self.device)
             if l1:
                 _check(lib().lob_process_messages_l1(self.ctx, _ptr(m), int(n_steps), int(msgs_per_step),
-                                                     _ptr(out) if l2 else None, _ptr(l1o), _stream(stream)),
+                                                     _ptr(out) if l2 else None, _ptr(l1o), st),
                        "lob_process_messages_l1")
             else:
                 _check(lib().lob_process_messages(self.ctx, _ptr(m), int(n_steps), int(msgs_per_step),
-                                                  _ptr(out) if l2 else None, _stream(stream)),
+                                                  _ptr(out) if l2 else None, st),
                        "lob_process_messages")
         self._keep = m
         if l1:
@@ -199,13 +226,23 @@ class LobBatch:
         return out if l2 else None
 
     def process_host(self, h_msgs, n_steps: int, msgs_per_step: int, h_l2_out=None,
-                     h_stats_out=None, d_msgs_buf=None, d_l2_buf=None, chunks: int = 8, stream=None):
-        """lob_process_messages_host: pinned host messages in, pinned host L2/stats out."""
+                     h_stats_out=None, d_msgs_buf=None, d_l2_buf=None, chunks: int = 8, stream=None,
+                     h_trades_out=None, h_trade_counts_out=None):
+        """lob_process_messages_host: pinned host messages in; pinned host L2 [K][S][L][4],
+        counters [K][10], and the LOGGED trade rows packed book after book into
+        ``h_trades_out`` (capacity [K*T_cap][6]) with per-book counts in
+        ``h_trade_counts_out`` [K].  The caller synchronises the stream before reading."""
         assert h_msgs.device.type == "cpu" and h_msgs.dtype == torch.int32 and h_msgs.is_contiguous()
-        with torch.cuda.device(self.device):
+        for t in (h_l2_out, h_stats_out, h_trades_out, h_trade_counts_out):
+            assert t is None or (t.device.type == "cpu" and t.is_contiguous() and t.is_pinned())
+        if h_trades_out is not None:
+            assert h_trades_out.dtype == torch.int32 and h_trades_out.numel() >= self.K * self.T_cap * 6
+            assert h_trade_counts_out is not None and h_trade_counts_out.numel() == self.K
+        with _On(self.device, stream) as st:
             _check(lib().lob_process_messages_host(
                 self.ctx, _ptr(h_msgs), int(n_steps), int(msgs_per_step), _ptr(h_l2_out),
-                _ptr(h_stats_out), _ptr(d_msgs_buf), _ptr(d_l2_buf), int(chunks), _stream(stream)),
+                _ptr(h_stats_out), _ptr(h_trades_out), _ptr(h_trade_counts_out), _ptr(d_msgs_buf),
+                _ptr(d_l2_buf), int(chunks), st),
                 "lob_process_messages_host")
 
     def step_reward(self, agent_oids, p_init, task_side, lam: float, stream=None):
@@ -213,51 +250,50 @@ class LobBatch:
 
         agent_oids [K][2] int32 (inclusive OID range), p_init [K] f64, task_side [K]
         int32 (-1 sell, +1 buy).  Returns (reward f64[K], vwap f64[K], agent_qty i64[K])."""
-        a = self._dev(agent_oids)
-        pi = self._dev(p_init, torch.float64)
-        sd = self._dev(task_side)
-        r = torch.empty((self.K,), dtype=torch.float64, device=self.device)
-        v = torch.empty_like(r)
-        q = torch.empty((self.K,), dtype=torch.int64, device=self.device)
-        with torch.cuda.device(self.device):
+        with _On(self.device, stream) as st:
+            a = self._dev(agent_oids)
+            pi = self._dev(p_init, torch.float64)
+            sd = self._dev(task_side)
+            r = torch.empty((self.K,), dtype=torch.float64, device=self.device)
+            v = torch.empty_like(r)
+            q = torch.empty((self.K,), dtype=torch.int64, device=self.device)
             _check(lib().lob_step_reward(self.ctx, _ptr(a), _ptr(pi), _ptr(sd), float(lam), _ptr(r), _ptr(v),
-                                         _ptr(q), _stream(stream)), "lob_step_reward")
+                                         _ptr(q), st), "lob_step_reward")
         self._keep = (a, pi, sd)
         return r, v, q
 
     def l2(self, stream=None):
-        out = torch.empty((self.K, self.L, 4), dtype=torch.int32, device=self.device)
-        with torch.cuda.device(self.device):
-            _check(lib().lob_get_l2(self.ctx, _ptr(out), _stream(stream)), "lob_get_l2")
+        with _On(self.device, stream) as st:
+            out = torch.empty((self.K, self.L, 4), dtype=torch.int32, device=self.device)
+            _check(lib().lob_get_l2(self.ctx, _ptr(out), st), "lob_get_l2")
         return out
 
     def trades(self, stream=None):
-        out = torch.empty((self.K, self.T_cap, 6), dtype=torch.int32, device=self.device)
-        cnt = torch.empty((self.K,), dtype=torch.int32, device=self.device)
-        with torch.cuda.device(self.device):
-            _check(lib().lob_get_trades(self.ctx, _ptr(out), _ptr(cnt), _stream(stream)),
-                   "lob_get_trades")
+        with _On(self.device, stream) as st:
+            out = torch.empty((self.K, self.T_cap, 6), dtype=torch.int32, device=self.device)
+            cnt = torch.empty((self.K,), dtype=torch.int32, device=self.device)
+            _check(lib().lob_get_trades(self.ctx, _ptr(out), _ptr(cnt), st), "lob_get_trades")
         return out, cnt
 
     def book(self, stream=None):
-        out = torch.empty((self.K, 2, self.N, 6), dtype=torch.int32, device=self.device)
-        with torch.cuda.device(self.device):
-            _check(lib().lob_get_book(self.ctx, _ptr(out), _stream(stream)), "lob_get_book")
+        with _On(self.device, stream) as st:
+            out = torch.empty((self.K, 2, self.N, 6), dtype=torch.int32, device=self.device)
+            _check(lib().lob_get_book(self.ctx, _ptr(out), st), "lob_get_book")
         return out
 
     def stats(self, stream=None):
-        out = torch.empty((self.K, LOB_NSTATS), dtype=torch.int64, device=self.device)
-        with torch.cuda.device(self.device):
-            _check(lib().lob_get_stats(self.ctx, _ptr(out), _stream(stream)), "lob_get_stats")
+        with _On(self.device, stream) as st:
+            out = torch.empty((self.K, LOB_NSTATS), dtype=torch.int64, device=self.device)
+            _check(lib().lob_get_stats(self.ctx, _ptr(out), st), "lob_get_stats")
         return out
 
 
     def digest(self, stream=None):
         """[K] per-book FNV-1a-64 of the exported book, trade log, n_trades and counters
         (lob_digest), as int64 bit patterns (torch has no uint64 arithmetic)."""
-        out = torch.empty((self.K,), dtype=torch.int64, device=self.device)
-        with torch.cuda.device(self.device):
-            _check(lib().lob_digest(self.ctx, _ptr(out), _stream(stream)), "lob_digest")
+        with _On(self.device, stream) as st:
+            out = torch.empty((self.K,), dtype=torch.int64, device=self.device)
+            _check(lib().lob_digest(self.ctx, _ptr(out), st), "lob_digest")
         return out
 
 
@@ -276,19 +312,19 @@ class LobEnv:
         self.executed = torch.empty((batch.K,), dtype=torch.int64, device=batch.device)
 
     def reset(self, init_ts: int, init_tns: int = 0, stream=None):
-        with torch.cuda.device(self.b.device):
+        with _On(self.b.device, stream) as st:
             _check(lib().lob_env_reset(self.b.ctx, _ptr(self.state), ctypes.byref(self.cfg), int(init_ts),
-                                       int(init_tns), _stream(stream)), "lob_env_reset")
+                                       int(init_tns), st), "lob_env_reset")
 
     def step(self, actions, data, l2_out=None, stream=None):
         """actions [K][4] f32, data [K][M][8] int32 -> (reward, done, executed) device tensors;
         ``self.work[:, :8]`` holds the agent's messages of the step."""
-        a = self.b._dev(actions, torch.float32)
-        d = self.b._dev(data)
-        assert a.shape == (self.b.K, 4) and d.shape == (self.b.K, self.M, 8)
-        with torch.cuda.device(self.b.device):
+        with _On(self.b.device, stream) as st:
+            a = self.b._dev(actions, torch.float32)
+            d = self.b._dev(data)
+            assert a.shape == (self.b.K, 4) and d.shape == (self.b.K, self.M, 8)
             _check(lib().lob_env_step(self.b.ctx, _ptr(self.state), ctypes.byref(self.cfg), _ptr(a), _ptr(d),
                                       self.M, _ptr(self.work), _ptr(self.reward), _ptr(self.done),
-                                      _ptr(self.executed), _ptr(l2_out), _stream(stream)), "lob_env_step")
+                                      _ptr(self.executed), _ptr(l2_out), st), "lob_env_step")
         self._keep = (a, d)
         return self.reward, self.done, self.executed

@@ -54,8 +54,9 @@ def test_state_bytes_host_only(L):
     n = L.lob_state_bytes(ctypes.byref(cfg))
     book = 65536 * 2 * 6 * 128 * 4
     trades = 65536 * 512 * 24
-    assert n >= book + trades + 65536 * 4 + 65536 * 80
-    assert n < book + trades + 65536 * 4 + 65536 * 80 + 4 * 256
+    tro = (65536 + 1) * 8     # host path: packed-trade row offsets + running total
+    assert n >= book + trades + 65536 * 4 + 65536 * 80 + tro
+    assert n < book + trades + 65536 * 4 + 65536 * 80 + tro + 5 * 256
     for bad in [(1, 0, 1, 10, 0), (1, 2049, 1, 10, 0), (1, 100, 1, 0, 0), (1, 100, 1, 33, 0),
                 (-1, 100, 1, 10, 0), (1, 100, -1, 10, 0)]:
         assert L.lob_state_bytes(ctypes.byref(lob._Config(*bad))) == 0, bad

@@ -181,8 +181,34 @@ def test_cuda_graph_mode_a(K):
     np.testing.assert_array_equal(tr.cpu().numpy(), want["trades"])
 
 
-def test_host_path_equals_device_path():
-    cfg = lobgen.CONFIGS["C4"].with_(n_books=3000)
+def _host_buffers(cfg):
+    K, S, L = cfg.n_books, cfg.n_steps, cfg.l2_levels
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory()
+    return {"l2": pin((K, S, L, 4), torch.int32), "st": pin((K, 10), torch.int64),
+            "tr": pin((K * cfg.trades_cap, 6), torch.int32), "cnt": pin((K,), torch.int32)}
+
+
+def _check_host_outputs(h, a, l2a):
+    """Host outputs of lob_process_messages_host against the device path `a`."""
+    assert torch.equal(h["l2"], l2a.cpu())
+    assert torch.equal(h["st"], a.stats().cpu())
+    tr, cnt = a.trades()
+    cnt = cnt.cpu()
+    assert torch.equal(h["cnt"], cnt)
+    n = int(cnt.sum())
+    mask = torch.arange(tr.shape[1])[None, :] < cnt[:, None]          # logged rows, book order
+    assert torch.equal(h["tr"][:n], tr.cpu()[mask])
+
+
+@pytest.mark.parametrize("name,n,chunks,Tcap", [("C4", 3000, 5, None), ("C3", 1200, 3, None),
+                                                ("C3", 700, 1, 2), ("C5_512", 150, 4, None)])
+def test_host_path_equals_device_path(name, n, chunks, Tcap):
+    """The end-to-end call (pinned host buffers in and out, chunked copy/compute pipeline)
+    returns exactly what the device path produces: per-step L2, counters, and every
+    logged trade row packed book after book with its per-book count (Eq.3-4)."""
+    cfg = lobgen.CONFIGS[name].with_(n_books=n)
+    if Tcap is not None:
+        cfg = cfg.with_(trades_cap=Tcap)
     msgs, init = lobgen.generate(cfg)
     from paper_2308_13289_b200 import LobBatch
     a = LobBatch(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
@@ -191,16 +217,90 @@ def test_host_path_equals_device_path():
     a.init(ti, lobgen.INIT_TS, lobgen.INIT_TNS)
     b.init(ti, lobgen.INIT_TS, lobgen.INIT_TNS)
     l2a = a.process(torch.from_numpy(msgs), cfg.n_steps, cfg.msgs_per_step)
-    h = torch.from_numpy(msgs).pin_memory()
-    hl2 = torch.empty((cfg.n_books, cfg.n_steps, cfg.l2_levels, 4), dtype=torch.int32).pin_memory()
-    hst = torch.empty((cfg.n_books, 10), dtype=torch.int64).pin_memory()
-    dm = torch.empty_like(h, device="cuda")
-    dl = torch.empty_like(hl2, device="cuda")
-    b.process_host(h, cfg.n_steps, cfg.msgs_per_step, hl2, hst, dm, dl, chunks=5)
+    hm = torch.from_numpy(msgs).pin_memory()
+    h = _host_buffers(cfg)
+    h["tr"].fill_(-7)
+    dm = torch.empty_like(hm, device="cuda")
+    dl = torch.empty_like(h["l2"], device="cuda")
+    b.process_host(hm, cfg.n_steps, cfg.msgs_per_step, h["l2"], h["st"], dm, dl, chunks=chunks,
+                   h_trades_out=h["tr"], h_trade_counts_out=h["cnt"])
     torch.cuda.synchronize()
-    assert torch.equal(hl2, l2a.cpu())
-    assert torch.equal(hst, a.stats().cpu())
+    _check_host_outputs(h, a, l2a)
+    assert (h["tr"][int(h["cnt"].sum()):] == -7).all()            # nothing past the packed rows
     assert torch.equal(b.book(), a.book())
+    # a second call continues the books (counters accumulate, the trade log is per call)
+    l2a = a.process(torch.from_numpy(msgs), cfg.n_steps, cfg.msgs_per_step)
+    b.process_host(hm, cfg.n_steps, cfg.msgs_per_step, h["l2"], h["st"], dm, dl, chunks=chunks,
+                   h_trades_out=h["tr"], h_trade_counts_out=h["cnt"])
+    torch.cuda.synchronize()
+    _check_host_outputs(h, a, l2a)
+
+
+def test_host_path_in_cuda_graph():
+    """lob_init + lob_process_messages_host captured once into a CUDA graph (the context's
+    copy streams fork from and join back to the capturing stream) and replayed: every
+    replay returns the device path's outputs in the host buffers."""
+    cfg = lobgen.CONFIGS["C4"].with_(n_books=2000)
+    msgs, init = lobgen.generate(cfg)
+    from paper_2308_13289_b200 import LobBatch
+    a = LobBatch(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
+    a.init(torch.from_numpy(init), lobgen.INIT_TS, lobgen.INIT_TNS)
+    l2a = a.process(torch.from_numpy(msgs), cfg.n_steps, cfg.msgs_per_step)
+    b = LobBatch(cfg.n_books, cfg.capacity, cfg.trades_cap, cfg.l2_levels)
+    hm = torch.from_numpy(msgs).pin_memory()
+    ti = torch.from_numpy(init).cuda()
+    h = _host_buffers(cfg)
+    dm = torch.empty_like(hm, device="cuda")
+    dl = torch.empty_like(h["l2"], device="cuda")
+
+    def run():
+        b.init(ti, lobgen.INIT_TS, lobgen.INIT_TNS)
+        b.process_host(hm, cfg.n_steps, cfg.msgs_per_step, h["l2"], h["st"], dm, dl, chunks=4,
+                       h_trades_out=h["tr"], h_trade_counts_out=h["cnt"])
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        run()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run()
+    for _ in range(2):
+        for t in h.values():
+            t.fill_(-5)
+        g.replay()
+        torch.cuda.synchronize()
+        _check_host_outputs(h, a, l2a)
+
+
+def test_host_trades_need_pinned_memory():
+    from paper_2308_13289_b200 import LobBatch, lib
+    import ctypes
+    cfg = lobgen.CONFIGS["C1"].with_(n_books=4)
+    msgs, init = lobgen.generate(cfg)
+    b = LobBatch(4, 100, cfg.trades_cap, 10)
+    b.init(torch.from_numpy(init), lobgen.INIT_TS, lobgen.INIT_TNS)
+    hm = torch.from_numpy(msgs).pin_memory()
+    dm = torch.empty_like(hm, device="cuda")
+    pageable = torch.empty((4 * cfg.trades_cap, 6), dtype=torch.int32)
+    cnt = torch.empty((4,), dtype=torch.int32).pin_memory()
+    rc = lib().lob_process_messages_host(b.ctx, ctypes.c_void_p(hm.data_ptr()), 10, 100, None, None,
+                                         ctypes.c_void_p(pageable.data_ptr()), ctypes.c_void_p(cnt.data_ptr()),
+                                         ctypes.c_void_p(dm.data_ptr()), None, 2,
+                                         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == -1 and b"pinned" in lib().lob_last_error()
+
+
+def test_env_rejects_agent_oid_base_zero():
+    from paper_2308_13289_b200 import EnvConfig, LobBatch, LobEnv, LobError
+    b = LobBatch(2, 16, 16, 2)
+    b.init(None, 0, 0)
+    env = LobEnv(b, EnvConfig(task_side=-1, task_size=10, n_passive=1, tick=10, episode_s=60, agent_tid=1,
+                              agent_oid_base=0, reserved=0, lam=0.0), 1)
+    with pytest.raises(LobError):
+        env.reset(34200, 0)
 
 
 @pytest.mark.parametrize("name", ["C4", "C3", "C5_32", "C5_100", "C5_512", "C5_2048"])

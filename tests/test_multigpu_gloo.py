@@ -80,3 +80,58 @@ def test_shard_ranges():
     assert all(rs[i][0] + rs[i][1] == rs[i + 1][0] for i in range(7))
     with pytest.raises(ValueError):
         shard_books(2, 2, 10)
+
+
+def _bench(args, env_extra):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **env_extra)
+    env.pop("WORLD_SIZE", None)
+    env.pop("RANK", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, env=env, capture_output=True,
+                         text=True, timeout=300)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    return out.returncode, [json.loads(l) for l in lines], out.stderr
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_bench_spawns_its_own_ranks(n):
+    """`bench.py --gpus N` without torchrun re-launches itself with N ranks (one process
+    per GPU) under torch.distributed.run; every rank checks WORLD_SIZE == N; rank 0 alone
+    prints.  Dry run: gloo, no GPU work."""
+    rc, lines, err = _bench(["--gpus", str(n)], {"LOB_BENCH_DRYRUN": "1", "LOB_DIST_BACKEND": "gloo"})
+    assert rc == 0, err[-2000:]
+    assert len(lines) == 1, lines
+    assert lines[0]["n_gpus"] == n and lines[0]["communicator_size"] == n
+    assert lines[0]["rank_sum"] == n * (n - 1) // 2
+
+
+def test_bench_refuses_world_size_mismatch():
+    """A launcher that starts fewer ranks than --gpus asks for is an error, not a silent
+    one-GPU measurement."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LOB_BENCH_DRYRUN="1", WORLD_SIZE="1", RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4"], env=env,
+                         capture_output=True, text=True, timeout=120)
+    assert out.returncode != 0 and "one rank per GPU" in out.stderr
+
+
+def test_bench_config_dicts_match_between_arms():
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    import lobgen
+    for argv in (["--gpus", "1"], ["--gpus", "8", "--scaling", "strong"], ["--gpus", "2", "--books", "1000"]):
+        a = bench.parse(argv)
+        cfg = lobgen.CONFIGS[a.config]
+        c = bench.config_dict(cfg, a, a.gpus)
+        assert c["books_total"] == (c["books_per_gpu"] * a.gpus if a.scaling == "weak" else
+                                    (a.books or cfg.n_books))
+    a = bench.parse(["--gpus", "8", "--scaling", "strong"])
+    assert bench.config_dict(lobgen.CONFIGS["C4"], a, 8)["books_per_gpu"] == 8192   # SURVEY 8(e)

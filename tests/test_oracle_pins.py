@@ -27,9 +27,9 @@ def test_golden(cid, case):
 
 
 # ------------------------------------------------- independent FIFO sorted map
-def _compare_with_fifo(cfg, n_books):
-    msgs, init = lobgen.generate(cfg.with_(n_books=n_books))
-    o = oracle.OracleBatch(n_books, cfg.capacity, cfg.n_msgs * 4, cfg.l2_levels, check=True)
+def _compare_with_fifo(cfg, n_books, make=oracle.OracleBatch, book_begin=0):
+    msgs, init = lobgen.generate(cfg.with_(n_books=n_books), book_begin=book_begin)
+    o = make(n_books, cfg.capacity, cfg.n_msgs * 4, cfg.l2_levels, check=True)
     o.init(init, lobgen.INIT_TS, lobgen.INIT_TNS)
     l2 = o.process(msgs, cfg.n_steps, cfg.msgs_per_step)
     tr, cnt = o.trades()
