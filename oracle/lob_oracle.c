@@ -295,8 +295,9 @@ static void process(oracle_ctx *X, obook *b, const int32_t *m) {
 }
 
 /* L2 top-L (G23): k-th best distinct price per side with its summed quantity;
- * absent levels are (-1, 0).  The sum is taken in int64 and reported as its
- * low 32 bits (two's complement); generator profiles keep it < 2^31 (G20). */
+ * absent levels are (-1, 0).  The sum is taken in int64; the record's fields are
+ * 32-bit, so a level volume above INT32_MAX is reported as INT32_MAX
+ * (saturated: "at least 2^31 - 1"; reading G20).  Generator profiles keep sums < 2^31. */
 static void l2_levels(oracle_ctx *X, const obook *b, int32_t *out /*[L][4]*/, int L) {
     int N = X->N;
     for (int s = 0; s < 2; s++) {
@@ -323,7 +324,7 @@ static void l2_levels(oracle_ctx *X, const obook *b, int32_t *out /*[L][4]*/, in
                     if (occupied(o) && o[O_P] == best) sum += o[O_Q];
                 }
                 price = best;
-                qty = (int32_t)(uint32_t)(uint64_t)sum;
+                qty = sum > INT32_MAX_ ? INT32_MAX_ : (int32_t)sum;
                 prev = best;
                 have_prev = 1;
             }

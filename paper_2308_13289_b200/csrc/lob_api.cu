@@ -538,6 +538,15 @@ int64_t lob_launch_count(void) { return g_launches.load(); }
 #endif
 const char *lob_build_id(void) { return LOB_BUILD_ID; }
 
+#ifdef LOB_TRACE_CYCLES
+// instrumented variant only (not in include/lob.h): copy the cycle trace of the last launch
+int lob_trace_read(int64_t *h_msg, int64_t *h_l2) {
+    cudaError_t e = cudaMemcpyFromSymbol(h_msg, g_trace_msg, sizeof(g_trace_msg));
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(h_l2, g_trace_l2, sizeof(g_trace_l2));
+    return e == cudaSuccess ? LOB_OK : cuda_fail(e, "trace read");
+}
+#endif
+
 const char *lob_strerror(int code) {
     switch (code) {
         case LOB_OK: return "ok";

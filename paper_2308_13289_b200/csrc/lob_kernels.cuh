@@ -360,7 +360,8 @@ struct Engine {
     static constexpr bool kBtRegs = (W > 1);
     int bTS[2], bTNS[2];
     int hr[2];              // row high-water mark per side (see with_rows)
-    unsigned bV[2];         // TL1: total quantity at the cached best price (its L1 volume)
+    unsigned long long bV[2];  // TL1: total quantity at the cached best price (its L1 volume,
+                               // exact in 64 bits; reported saturated at INT32_MAX, G20)
     long long part_cxl;     // cancelled quantity, accumulated on the owner thread (G14)
     long long part_trd;     // traded quantity, accumulated on the owner thread
 
@@ -399,6 +400,21 @@ struct Engine {
         const unsigned r = __reduce_add_sync(FULL, x);
         if constexpr (W == 1) return r;
         else return __reduce_add_sync(FULL, exchange(r, 0u));
+    }
+    // exact group sum of per-thread partials < 2^35 (sums of up to 16 int32 quantities):
+    // two 32-bit reductions of the high and low 16-bit halves (each total < 2^27)
+    __device__ __forceinline__ unsigned long long gadd64(unsigned long long x) {
+        const unsigned hi = gadd((unsigned)(x >> 16)), lo = gadd((unsigned)(x & 0xffffu));
+        return ((unsigned long long)hi << 16) + lo;
+    }
+    // any thread of the group
+    __device__ __forceinline__ bool gany(bool x) {
+        if constexpr (W == 1) return __any_sync(FULL, x);
+        else return gmin_u(x ? 0u : 1u) == 0u;
+    }
+    // a level volume as reported (G20): the exact sum saturated at INT32_MAX
+    static __device__ __forceinline__ int sat32(unsigned long long v) {
+        return v > (unsigned long long)INT_MAX ? INT_MAX : (int)v;
     }
     // value held by thread `owner` of the group, to every thread
     __device__ __forceinline__ int bcast(int x, int owner) {
@@ -497,7 +513,7 @@ struct Engine {
         if (m == 0xffffffffu) { set_empty<SD>(); return; }
         // candidates at the best price: thread-local earliest (Ts, Tns, row)
         int lts = INT_MAX, ltns = INT_MAX, lj = -1, lc = 0;
-        unsigned lv = 0;
+        unsigned long long lv = 0;
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
@@ -506,10 +522,10 @@ struct Engine {
                 const int2 t2 = bk.times(SD, j * GT + tid);
                 if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
                 ++lc;
-                lv += (unsigned)q;
+                if constexpr (TL1) lv += (unsigned)q;
             }
         }
-        if constexpr (TL1) bV[SD] = gadd(lv);
+        if constexpr (TL1) bV[SD] = gadd64(lv);
         const unsigned loc = lj < 0 ? 0xffffffffu : (unsigned)(lj * GT + tid);
         int slot;
         if (gadd((unsigned)lc) == 1) {
@@ -543,7 +559,7 @@ struct Engine {
         const unsigned m = gmin_u(lk);
         if (m == 0xffffffffu) { set_empty<SD>(); return; }
         int lts = INT_MAX, ltns = INT_MAX, lj = -1;
-        unsigned lv = 0;
+        unsigned long long lv = 0;
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const int q = bk.hot(SD, F_Q, j), p = bk.hot(SD, F_P, j);
@@ -551,10 +567,10 @@ struct Engine {
             if (q > 0 && k == m) {
                 const int2 t2 = bk.times(SD, j * GT + tid);
                 if (lj < 0 || t2.x < lts || (t2.x == lts && t2.y < ltns)) { lts = t2.x; ltns = t2.y; lj = j; }
-                lv += (unsigned)q;
+                if constexpr (TL1) lv += (unsigned)q;
             }
         }
-        if constexpr (TL1) bV[SD] = gadd(lv);
+        if constexpr (TL1) bV[SD] = gadd64(lv);
         const bool in = lj >= 0;
         const int w1 = __reduce_min_sync(FULL, in ? lts : INT_MAX);
         const bool in1 = in && lts == w1;
@@ -649,7 +665,7 @@ struct Engine {
         bk.template put_if_r<R>(own, SD, F_Q, j, qi - mQ);  // Q <= 0 -> empty
         if constexpr (TL1) {                       // the level volume loses what was cancelled there
             const int d = bcast(bk.get(SD, F_P, j) == bP[SD] ? cq : 0, slot & (GT - 1));
-            if (bslot[SD] >= 0) bV[SD] -= (unsigned)d;
+            if (bslot[SD] >= 0) bV[SD] -= (unsigned long long)d;
         }
         if (bslot[SD] == slot) bslot[SD] = BEST_INVALID;
     }
@@ -707,7 +723,7 @@ struct Engine {
             }
             ++ntr;                                                   // fills this call (logged = min(ntr, Tcap))
             bk.template put_if_r<R>(own, OPP, F_Q, sj, Qs2);         // filled order removed (G10)
-            if constexpr (TL1) bV[OPP] -= (unsigned)q;
+            if constexpr (TL1) bV[OPP] -= (unsigned long long)q;
             if (Qs2 == 0) bslot[OPP] = BEST_INVALID;
         }
         return Qa;
@@ -752,7 +768,7 @@ struct Engine {
             const int ob = bslot[OWN], op = bP[OWN];
             const bool lvl = ob == BEST_EMPTY || (ob >= 0 && ((OWN == ASK) ? mP < op : mP > op));
             const bool same = ob >= 0 && mP == op;
-            bV[OWN] = lvl ? (unsigned)Qa : (same ? bV[OWN] + (unsigned)Qa : bV[OWN]);
+            bV[OWN] = lvl ? (unsigned long long)Qa : (same ? bV[OWN] + (unsigned long long)Qa : bV[OWN]);
         }
         note_add<OWN>(slot, mP, mTS, mTNS, Qa);
     }
@@ -764,7 +780,8 @@ struct Engine {
         if (bslot[BID] == BEST_INVALID) recompute_best<BID>();
         const bool a = bslot[ASK] >= 0, b = bslot[BID] >= 0;
         // predicated store (no lane-divergent branch in the message loop)
-        stg128_if0(tid, dst, make_int4(a ? bP[ASK] : -1, a ? (int)bV[ASK] : 0, b ? bP[BID] : -1, b ? (int)bV[BID] : 0));
+        stg128_if0(tid, dst,
+                   make_int4(a ? bP[ASK] : -1, a ? sat32(bV[ASK]) : 0, b ? bP[BID] : -1, b ? sat32(bV[BID]) : 0));
     }
 
     // A message whose first word holds its dispatch code (msg_code) instead of T.
@@ -824,13 +841,32 @@ struct Engine {
             if (tid == k) { outp = (SD == ASK) ? (int)(m + 1u) : (int)(INT_MAX - (int)m); outq = (int)qs; }
         }
     }
-    // L2 over the first R rows only (with_rows)
+    // L2 over the first R rows only (with_rows).  Volume (G20): the exact sum, saturated
+    // at INT32_MAX.  While every resting Q on the side is below 2^20 no level can reach
+    // 2^31 (N <= 2048) and the 32-bit sums above are exact; otherwise (one vote per
+    // snapshot decides, uniformly) the volumes are recomputed in 64 bits -- a rare path
+    // kept outside the row-specialised code.
     template <int SD>
     __device__ __forceinline__ void l2_side(int L, int &outp, int &outq) {
         outp = -1; outq = 0;
         const int h = hr[SD];
         if (h < 0) return;
         with_rows(h, [&](auto R) { l2_rows<SD, R>(L, outp, outq); });
+        bool bg = false;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) bg |= bk.hot(SD, F_Q, j) >= (1 << 20);
+        if (gany(bg)) {
+            for (int k = 0; k < L; ++k) {
+                const int pk = bcast(tid == k ? outp : 0, k);   // level k's price (-1: absent)
+                if (pk < 0) break;
+                unsigned long long l64 = 0;
+#pragma unroll
+                for (int j = 0; j < KPL; ++j)
+                    if (bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_P, j) == pk) l64 += (unsigned)bk.hot(SD, F_Q, j);
+                const int v = sat32(gadd64(l64));
+                if (tid == k) outq = v;
+            }
+        }
     }
     __device__ __forceinline__ void l2_write(int32_t *dst, int L) {
         int ap, aq, bp, bq;
@@ -989,6 +1025,14 @@ __device__ __forceinline__ void env_post(const Params &p, const EnvParams &ep, i
     else if (tid < 32) env_post_warp(p, ep, b, tid, n, have_last, last_ts, last_tns);
 }
 
+#ifdef LOB_TRACE_CYCLES
+// instrumented variant only: clock64 at the start of every message and around every L2
+// snapshot of the first LOB_TRACE_BOOKS books of a launch (scripts/cycle_budget.py)
+constexpr int LOB_TRACE_BOOKS = 8, LOB_TRACE_MSGS = 10240, LOB_TRACE_STEPS = 128;
+__device__ long long g_trace_msg[LOB_TRACE_BOOKS][LOB_TRACE_MSGS];
+__device__ long long g_trace_l2[LOB_TRACE_BOOKS][LOB_TRACE_STEPS][2];
+#endif
+
 // Dynamic shared memory of one CTA of G books of (KPL, W).
 template <int KPL, int W, int G>
 constexpr int step_smem_bytes() {
@@ -1105,6 +1149,12 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
                 const uint32_t mend = maddr + 32u * run;
                 do {
                     const int4 a = lds128(maddr), bb = lds128(maddr + 16);
+#ifdef LOB_TRACE_CYCLES  // instrumented variant only (scripts/cycle_budget.py): message start times
+                    if (tid == 0 && lb < LOB_TRACE_BOOKS) {
+                        const int mi = c * CH + (int)((maddr - (stage + slot * CH * 32)) >> 5);
+                        if (mi < LOB_TRACE_MSGS) g_trace_msg[lb][mi] = clock64();
+                    }
+#endif
                     if constexpr (ENV) {
                         if (!idle) {
                             e.message_coded(a, bb);
@@ -1123,7 +1173,16 @@ __global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (
                 left -= run;
                 if (left == 0) {  // end of a step: L2 snapshot (G23)
                     left = p.M;
+#ifdef LOB_TRACE_CYCLES
+                    const long long tl0 = clock64();
+#endif
                     if (p.l2out) e.l2_write(p.l2out + (((size_t)lb * p.n_steps + step) * p.L) * 4, p.L);
+#ifdef LOB_TRACE_CYCLES
+                    if (tid == 0 && lb < LOB_TRACE_BOOKS && step < LOB_TRACE_STEPS) {
+                        g_trace_l2[lb][step][0] = tl0;
+                        g_trace_l2[lb][step][1] = clock64();
+                    }
+#endif
                     ++step;
                 }
             }

@@ -3,7 +3,7 @@
 # so the dynamic book scheduler runs under racecheck/synccheck, and the many-wave build.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-for tool in memcheck racecheck synccheck; do
+for tool in memcheck racecheck synccheck initcheck; do
   for cap in 0 1; do
     LOB_GRID_CAP=$cap timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize.py > gpurun_out/san_${tool}_cap$cap.txt 2>&1
     echo "$tool cap=$cap rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|hazard' gpurun_out/san_${tool}_cap$cap.txt | tail -1)"

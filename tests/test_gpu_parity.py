@@ -647,3 +647,48 @@ def test_capacity_saturated(monkeypatch, N, wide):
     assert (ov > 0).mean() >= 0.5, "the stream must overflow most books"
     occ = (o["book"][..., 1] > 0).sum(-1)
     assert (occ <= N).all() and (occ.max() == N)
+
+
+def _big_qty_stream(rng, n):
+    """Limits with quantities up to max_int at a handful of prices (level volumes far past
+    2^31), partial cancels and small market orders: the saturating L2 / L1 volume (G20)."""
+    out = np.zeros((n, 8), np.int32)
+    for i in range(n):
+        S = int(rng.choice([-1, 1]))
+        ts, tns = 34200 + i, 0
+        k = rng.integers(0, 10)
+        if k < 7:
+            P = 1000 + S * -10 * int(rng.integers(1, 4))          # passive: asks above 1000, bids below
+            Q = int(rng.choice([rng.integers(1 << 27, 2**31 - 1), rng.integers(1, 1 << 20)]))
+            out[i] = (1, S, Q, P, i + 1, 7, ts, tns)
+        elif k < 9:
+            out[i] = (2, S, int(rng.integers(1, 1 << 30)), 0, int(rng.integers(1, i + 2)), 7, ts, tns)
+        else:
+            out[i] = (4, S, int(rng.integers(1, 1 << 29)), 0, i + 1, 7, ts, tns)
+    return out
+
+
+@pytest.mark.parametrize("N,l1,wide", [(100, False, False), (100, True, False), (100, False, True), (7, True, False),
+                                       (300, False, False), (300, True, False), (1500, False, False),
+                                       (1500, True, False)])
+def test_l2_volume_saturation(monkeypatch, N, l1, wide):
+    if wide:
+        monkeypatch.setenv("LOB_FORCE_WIDE", "1")
+    K, S, M = 40, 8, 30
+    rng = np.random.default_rng(N + 11 * l1 + 5 * wide)
+    msgs = np.stack([_big_qty_stream(rng, S * M) for _ in range(K)])
+    g, o = GpuEngine(K, N, 64, 5), oracle.OracleBatch(K, N, 64, 5)
+    res = []
+    for e in (g, o):
+        e.init(None, 0, 0)
+        out = e.process(msgs, S, M, l2=True, l1=l1)
+        res.append((out, e.book(), e.stats(), e.l2()))
+    l2o = res[1][0][0] if l1 else res[1][0]
+    assert (l2o[..., 1] == 2**31 - 1).any() and (l2o[..., 3] == 2**31 - 1).any()    # saturated levels occur
+    assert (l2o[..., 1] >= 0).all() and (l2o[..., 3] >= 0).all()
+    for a, b, what in zip(res[0], res[1], ("out", "book", "stats", "l2_now")):
+        if what == "out" and l1:
+            np.testing.assert_array_equal(a[0], b[0], err_msg="l2")
+            np.testing.assert_array_equal(a[1], b[1], err_msg="l1")
+        else:
+            np.testing.assert_array_equal(a, b, err_msg=what)

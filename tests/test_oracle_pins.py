@@ -118,6 +118,90 @@ def test_bruteforce_all_sequences_up_to_3(N):
         assert st[k, ST["market_discarded_qty"]] == ref.discarded
 
 
+def _alphabet_array():
+    """The 40-message alphabet as rows [T, S, Q, P, OID or 0 (= position-dependent)]."""
+    T = {"L": 1, "C": 2, "D": 3, "M": 4}
+    return np.asarray([[T[k], S, Q, P, 0 if oid is None else oid] for k, S, Q, P, oid in _alphabet()], np.int64)
+
+
+def _encode_all(idx):
+    """Vectorised _encode for sequences given as alphabet indices idx [n][length]."""
+    a = _alphabet_array()
+    n, length = idx.shape
+    m = np.zeros((n, length, 8), np.int32)
+    rows = a[idx]                                          # [n][length][5]
+    pos = np.arange(1, length + 1)[None, :]
+    m[..., :4] = rows[..., :4]
+    m[..., 4] = np.where(rows[..., 4] == 0, pos, rows[..., 4])
+    m[..., 5] = 7
+    m[..., 6] = pos
+    return m
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("N", [1, 2, 3])
+def test_bruteforce_all_sequences_of_length_4(N):
+    """Every sequence of exactly 4 messages over the 40-message alphabet (2,560,000 per
+    capacity) in check mode: sentinel discipline, never crossed, priority of every fill,
+    quantity conservation, fills = logged + dropped, unknown cancels leave the book
+    bit-identical -- after every message.  (Shorter sequences: the length <= 3 test; at
+    N < 4 the sorted-map FIFO comparison needs N >= length, see the N = 4 sample below.)"""
+    n_alpha = len(_alphabet())
+    total = n_alpha ** 4
+    chunk = 160_000
+    for c0 in range(0, total, chunk):
+        flat = np.arange(c0, min(total, c0 + chunk))
+        idx = np.stack([(flat // n_alpha ** p) % n_alpha for p in (3, 2, 1, 0)], 1)
+        msgs = _encode_all(idx)
+        o = oracle.OracleBatch(len(flat), N, 4, 3, check=True, threads=8)
+        o.process(msgs, 4, 1, l2=False)
+        v = o.violations()
+        assert (v == 0).all(), (N, c0 + int(np.argmax(v)))
+        st = o.stats()
+        assert (st[:, ST["msgs"]] == 4).all()
+        occ = (o.book()[..., 1] > 0).sum(-1)
+        assert (occ <= N).all()
+
+
+@pytest.mark.slow
+def test_length_4_sample_equals_fifo_at_capacity_4():
+    """A seeded sample of 25,000 length-4 sequences at N = 4 (no overflow possible):
+    trade tape, per-step L2, unknown cancels and discarded market quantity equal the
+    independent sorted-map FIFO engine's."""
+    rng = np.random.default_rng(44)
+    idx = rng.integers(0, len(_alphabet()), (25_000, 4))
+    msgs = _encode_all(idx)
+    o = oracle.OracleBatch(len(idx), 4, 16, 3, check=True, threads=8)
+    l2 = o.process(msgs, 4, 1)
+    assert (o.violations() == 0).all()
+    tr, cnt = o.trades()
+    st = o.stats()
+    for k in range(len(idx)):
+        ref, snaps = run_stream(msgs[k], 4, 1, 3)
+        assert [tuple(t) for t in tr[k, :cnt[k]].tolist()] == ref.tape, k
+        np.testing.assert_array_equal(l2[k], np.asarray(snaps, np.int32))
+        assert st[k, ST["unknown_cancels"]] == ref.unknown
+        assert st[k, ST["market_discarded_qty"]] == ref.discarded
+
+
+def test_vectorised_encoding_matches_encode():
+    rng = np.random.default_rng(3)
+    alpha = _alphabet()
+    idx = rng.integers(0, len(alpha), (50, 4))
+    want = np.asarray([_encode([alpha[i] for i in row], 4) for row in idx], np.int32)
+    np.testing.assert_array_equal(_encode_all(idx), want)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("profile", ["lobster", "cancel_heavy", "heavy_market", "synthetic"])
+def test_oracle_equals_fifo_engine_1024_streams(profile):
+    """SPEC acceptance #1 at its stated size (>= 1000 random streams):
+    4 profiles x 256 streams = 1,024 streams of 1,000 messages at N = 100, global book ids
+    disjoint from the other FIFO tests."""
+    cfg = lobgen.Config("pin1k", 256, 100, 10, 100, 33 if profile != "lobster" else 10, 4000, 10, profile, 7001)
+    _compare_with_fifo(cfg, 256, book_begin=100_000)
+
+
 def test_bruteforce_random_longer_sequences():
     rng = np.random.default_rng(5)
     alpha = _alphabet()
@@ -283,3 +367,21 @@ def test_saturate_profile_reaches_capacity():
         assert (st[:, STAT_NAMES.index("add_overflow")] > 0).mean() >= 0.5, N
         occ = (o.book()[..., 1] > 0).sum(-1)
         assert occ.max() == N and (occ <= N).all(), N
+
+
+def test_l2_volume_saturates_at_int32_max():
+    """G20: a level's volume is the exact int64 sum reported in the int32 field, saturated
+    at INT32_MAX (32-bit fields).  Closed forms: 1.5e9 + 6e8 = 2.1e9 fits; 2^30 +
+    2^30 = 2^31 does not (INT32_MAX); a level of three max-int orders is INT32_MAX, never a
+    wrapped (negative) value; level 1 of the L1 trace is the same number."""
+    IMAX = 2**31 - 1
+    rows = [[1, -1, 1_500_000_000, 105, 1, 0, 1, 0], [1, -1, 600_000_000, 105, 2, 0, 2, 0],
+            [1, -1, 2**30, 106, 3, 0, 3, 0], [1, -1, 2**30, 106, 4, 0, 4, 0],
+            [1, 1, IMAX, 90, 5, 0, 5, 0], [1, 1, IMAX, 90, 6, 0, 6, 0], [1, 1, IMAX, 90, 7, 0, 7, 0],
+            [1, 1, 5, 89, 8, 0, 8, 0]]
+    o = oracle.OracleBatch(1, 8, 4, 3, check=True)
+    l2, l1 = o.process(np.asarray(rows, np.int32)[None], 1, 8, l1=True)
+    assert l2[0, 0].tolist() == [[105, 2_100_000_000, 90, IMAX], [106, IMAX, 89, 5], [-1, 0, -1, 0]]
+    assert l1[0, -1].tolist() == [105, 2_100_000_000, 90, IMAX]
+    assert l1[0, 5].tolist() == [105, 2_100_000_000, 90, IMAX]       # two max-int bids: 2^32 - 2 -> IMAX
+    assert (o.violations() == 0).all()
