@@ -201,6 +201,39 @@ int lob_env_step(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const flo
                  const int32_t *d_data, int32_t msgs_per_step, int32_t *d_work, double *d_reward,
                  int32_t *d_done, int64_t *d_executed, int32_t *d_l2_out, void *cuda_stream);
 
+/* NEXT row N3, residency ("a persistent kernel ... for K <~ 7k";
+ * PAPER.md P:L414-423): a RESIDENT env session.  lob_session_begin launches ONE
+ * persistent kernel (on a stream owned by the context, forked from cuda_stream) that
+ * loads every book once and keeps it on chip for a whole episode; each
+ * lob_session_step(ctx, s) then runs exactly what one lob_env_step call runs (agent
+ * messages from d_actions, the step's data, the post-step L2, reward / done / executed)
+ * without reloading or storing any book, and lob_session_end writes the books and
+ * counters back.  Results are identical to calling lob_env_step once per step.
+ *  d_data [K][n_steps][msgs_per_step][8]: the whole episode's data messages, read-only
+ *    for the session's lifetime (streamed ahead of the steps);
+ *  d_actions [K][4] f32: READ AT EACH STEP -- the caller writes step s's actions into it
+ *    on cuda_stream before lob_session_step;
+ *  d_work, d_reward, d_done, d_executed, d_l2_out ([K][L][4], nullable): the same
+ *    outputs as lob_env_step, overwritten by every step, complete on cuda_stream after
+ *    lob_session_step returns (stream order).
+ * lob_session_step enqueues on cuda_stream a release of the next step (a stream memory
+ * write) and a wait until every book has finished it (a stream memory wait); the host
+ * does not block.  Between begin and end the trade log and its count are per step (as
+ * after a lob_env_step); the book (lob_get_book) and the counters are updated at end.
+ * Requirements: one session per context; msgs_per_step >= 1; every book resident at
+ * once (ceil(K / books per CTA) CTAs in one wave of the GPU, else LOB_EUNSUPPORTED; the
+ * launch is cooperative); at most n_steps steps (then LOB_EINVAL); the driver's stream
+ * memory operations (else LOB_EUNSUPPORTED).  Calls on the context other than
+ * lob_session_* while a session runs are undefined, and a DEVICE-wide synchronisation
+ * (cudaDeviceSynchronize) deadlocks: it waits for the resident kernel, which waits for
+ * the next step -- synchronise streams instead.  lob_destroy stops a running session. */
+int lob_session_begin(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const float *d_actions,
+                      const int32_t *d_data, int32_t n_steps, int32_t msgs_per_step, int32_t *d_work,
+                      double *d_reward, int32_t *d_done, int64_t *d_executed, int32_t *d_l2_out,
+                      void *cuda_stream);
+int lob_session_step(lob_ctx *ctx, void *cuda_stream);
+int lob_session_end(lob_ctx *ctx, void *cuda_stream);
+
 /* Current L2 snapshot of every book: d_out [K][L][4] int32. */
 int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *cuda_stream);
 

@@ -5,7 +5,7 @@ The product is ``liblob.so`` behind the C ABI in ``include/lob.h``; this package
 its thin binding.  See DESIGN.md.
 """
 from .lob import (LIB_PATH, LOB_NSTATS, MAX_CAPACITY, MAX_L2_LEVELS, STAT_NAMES, EnvConfig, LobBatch,
-                  LobEnv, LobError, build_id, launch_count, lib)
+                  LobEnv, LobError, LobSession, build_id, launch_count, lib)
 
-__all__ = ["LobBatch", "LobEnv", "EnvConfig", "LobError", "lib", "launch_count", "build_id", "LIB_PATH", "LOB_NSTATS",
+__all__ = ["LobBatch", "LobEnv", "LobSession", "EnvConfig", "LobError", "lib", "launch_count", "build_id", "LIB_PATH", "LOB_NSTATS",
            "STAT_NAMES", "MAX_CAPACITY", "MAX_L2_LEVELS"]

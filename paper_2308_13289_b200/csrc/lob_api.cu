@@ -2,6 +2,7 @@
 // Validation, state layout, launch configuration; all compute is in
 // lob_kernels.cuh.  No CPU fallback: every entry point either launches the
 // sm_100a kernels or returns an error.
+#include <cuda.h>  // driver types for the stream memory operations (entry points via the runtime)
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -13,6 +14,7 @@
 #include "../../include/lob.h"
 #include "lob_kernels.cuh"
 #include "lob_env.cuh"
+#include "lob_session.cuh"
 
 using namespace lobk;
 
@@ -55,7 +57,7 @@ Geo geo_of(int N) {
 
 struct Layout {
     int NP;
-    size_t off_book, off_trades, off_ntr, off_stats, off_sched, off_tro, total;
+    size_t off_book, off_trades, off_ntr, off_stats, off_sched, off_tro, off_sess, total;
 };
 
 bool layout_of(const lob_config *c, Layout *L) {
@@ -73,7 +75,9 @@ bool layout_of(const lob_config *c, Layout *L) {
     L->off_sched = al(L->off_stats + K * NST * sizeof(long long));
     // host path only: per-book row offsets of the packed trade copy + the running total
     L->off_tro = al(L->off_sched + 2 * sizeof(unsigned));
-    L->total = al(L->off_tro + (K + 1) * sizeof(long long));
+    // resident env session: the step flag and the finished book-step counter
+    L->off_sess = al(L->off_tro + (K + 1) * sizeof(long long));
+    L->total = al(L->off_sess + 2 * sizeof(unsigned));
     return true;
 }
 }  // namespace
@@ -92,14 +96,24 @@ struct lob_ctx {
     // and kept for the context's lifetime (none per call)
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_start = nullptr, ev_h = nullptr, ev_k = nullptr;
+    // resident env session (lob_session_*): its stream, the join event, the step count
+    cudaStream_t sess = nullptr;
+    cudaEvent_t ev_sess = nullptr;
+    bool sess_active = false;
+    int sess_step = 0, sess_nsteps = 0, sess_grid_cap = 0;
     int32_t *book() const { return reinterpret_cast<int32_t *>(state + lay.off_book); }
     int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
     int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
     long long *stats() const { return reinterpret_cast<long long *>(state + lay.off_stats); }
     unsigned *sched() const { return reinterpret_cast<unsigned *>(state + lay.off_sched); }
     long long *tro() const { return reinterpret_cast<long long *>(state + lay.off_tro); }
+    unsigned *sess_go() const { return reinterpret_cast<unsigned *>(state + lay.off_sess); }
+    unsigned *sess_done() const { return sess_go() + 1; }
 };
 
+#ifndef G16
+#define G16 4
+#endif
 namespace {
 // call f(IC<KPL>, IC<W>, IC<G>) for the compiled geometry (G = books per CTA)
 template <class F>
@@ -111,7 +125,7 @@ void for_geo(Geo g, F &&f) {
             case 3: f(IC<3>(), IC<1>(), IC<4>()); break;
             case 4: f(IC<4>(), IC<1>(), IC<4>()); break;
             case 8: f(IC<8>(), IC<1>(), IC<4>()); break;
-            default: f(IC<16>(), IC<1>(), IC<4>()); break;
+            default: f(IC<16>(), IC<1>(), IC<G16>()); break;
         }
     } else {
         if (g.kpl == 8) f(IC<8>(), IC<4>(), IC<1>());
@@ -205,7 +219,7 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
         const char *gc = getenv("LOB_GRID_CAP");
         c->grid_limit = gc ? atoi(gc) : 0;
     }
-    int per_sm[4] = {1, 1, 1, 1};
+    int per_sm[4] = {1, 1, 1, 1}, sess_per_sm = 0;
     int rc = LOB_OK;
     for_geo(c->geo, [&](auto kc, auto wc, auto gc) {
         constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, G = decltype(gc)::value;
@@ -229,18 +243,30 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
                                                                   smem);
         }
         if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(lob_session<KPL, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sess_per_sm, lob_session<KPL, W, G>, 32 * W * G, smem);
+        if (e == cudaSuccess)
             e = cudaFuncSetAttribute(lob_export_l2<KPL, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      export_l2_smem_bytes<KPL, W>());
         if (e != cudaSuccess) rc = cuda_fail(e, "kernel attribute / occupancy query");
     });
     if (rc != LOB_OK) { delete c; return rc; }
     for (int m = 0; m < 4; ++m) c->grid_cap[m] = sms * (per_sm[m] > 0 ? per_sm[m] : 1);
+    c->sess_grid_cap = sms * sess_per_sm;
     *out = c;
     return LOB_OK;
 }
 
 void lob_destroy(lob_ctx *ctx) {
     if (!ctx) return;
+    if (ctx->sess_active) {  // a session still running: stop it (synchronously) before the streams go
+        const unsigned stop = SESSION_STOP | (unsigned)ctx->sess_step;
+        cudaMemcpy(ctx->sess_go(), &stop, sizeof stop, cudaMemcpyHostToDevice);
+        cudaStreamSynchronize(ctx->sess);
+    }
+    if (ctx->sess) cudaStreamDestroy(ctx->sess);
+    if (ctx->ev_sess) cudaEventDestroy(ctx->ev_sess);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     for (cudaEvent_t e : {ctx->ev_start, ctx->ev_h, ctx->ev_k})
@@ -467,6 +493,130 @@ int lob_env_step(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const flo
     ep.executed = reinterpret_cast<long long *>(d_executed);
     // one fused launch: agent messages, the step's data, reward / time / termination
     return launch_step(ctx, d_data, 1, msgs_per_step, d_l2_out, 0, K, (cudaStream_t)stream, nullptr, &ep);
+}
+
+// ---------------------------------------------------------------- resident env session
+namespace {
+typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_write32 g_write32 = nullptr;
+PFN_wait32 g_wait32 = nullptr;
+
+// the driver's stream memory operations, through the runtime's entry-point query (no
+// link-time dependency on libcuda)
+int stream_memops() {
+    if (g_write32 && g_wait32) return LOB_OK;
+    void *w = nullptr, *t = nullptr;
+    cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = q1;
+    cudaError_t e = cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1);
+    if (e == cudaSuccess) e = cudaGetDriverEntryPoint("cuStreamWaitValue32", &t, cudaEnableDefault, &q2);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDriverEntryPoint");
+    if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !w || !t)
+        return fail(LOB_EUNSUPPORTED, "stream memory operations (cuStreamWriteValue32/cuStreamWaitValue32) unavailable%s");
+    g_write32 = reinterpret_cast<PFN_write32>(w);
+    g_wait32 = reinterpret_cast<PFN_wait32>(t);
+    return LOB_OK;
+}
+int cu_fail(CUresult r, const char *where) {
+    snprintf(g_err, sizeof(g_err), "%s: CUresult %d", where, (int)r);
+    return LOB_ECUDA;
+}
+}  // namespace
+
+int lob_session_begin(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const float *d_actions,
+                      const int32_t *d_data, int32_t n_steps, int32_t msgs_per_step, int32_t *d_work,
+                      double *d_reward, int32_t *d_done, int64_t *d_executed, int32_t *d_l2_out, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (ctx->sess_active) return fail(LOB_EINVAL, "a session is already running on this context%s");
+    if (!env_cfg_ok(cfg)) return fail(LOB_EINVAL, "invalid lob_env_config%s");
+    const int K = ctx->cfg.n_books;
+    if (K == 0) return fail(LOB_EINVAL, "a session needs at least one book%s");
+    if (n_steps < 1 || msgs_per_step < 1 || (long long)n_steps * msgs_per_step > (1ll << 30))
+        return fail(LOB_EINVAL, "bad n_steps/msgs_per_step%s");
+    if (!d_env || !d_actions || !d_data || !d_work)
+        return fail(LOB_EINVAL, "env, actions, data and work buffers are required%s");
+    if (reinterpret_cast<uintptr_t>(d_env) % 16 || reinterpret_cast<uintptr_t>(d_work) % 16 ||
+        reinterpret_cast<uintptr_t>(d_data) % 16 || reinterpret_cast<uintptr_t>(d_l2_out) % 16 ||
+        reinterpret_cast<uintptr_t>(d_reward) % 8 || reinterpret_cast<uintptr_t>(d_executed) % 8)
+        return fail(LOB_EINVAL, "misaligned buffer%s");
+    rc = stream_memops();
+    if (rc) return rc;
+    int G = 1;
+    for_geo(ctx->geo, [&](auto, auto, auto gc) { G = decltype(gc)::value; });
+    const long long grid = (K + G - 1) / G;
+    if (grid > ctx->sess_grid_cap)  // every book must stay resident: one wave only
+        return fail(LOB_EUNSUPPORTED, "too many books for a resident session (one wave of the GPU)%s");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (!ctx->sess) {
+        e = cudaStreamCreateWithFlags(&ctx->sess, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_sess, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "session stream / event creation");
+    }
+    e = cudaMemsetAsync(ctx->sess_go(), 0, 2 * sizeof(unsigned), st);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_sess, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->sess, ctx->ev_sess, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "session fork");
+    Params p;
+    p.book = ctx->book(); p.trades = ctx->trades(); p.ntrades = ctx->ntr(); p.stats = ctx->stats();
+    p.msgs = d_data; p.l2out = d_l2_out; p.l1out = nullptr; p.sched = ctx->sched();
+    p.N = ctx->cfg.capacity; p.NP = ctx->lay.NP; p.Tcap = ctx->cfg.trades_cap; p.L = ctx->cfg.l2_levels;
+    p.n_steps = 1; p.M = msgs_per_step; p.book0 = 0; p.nb = K;
+    EnvParams ep{};
+    memcpy(&ep.ec, cfg, sizeof ep.ec);
+    ep.env = static_cast<EnvState *>(d_env);
+    ep.actions = d_actions;
+    ep.agent_out = d_work;
+    ep.reward = d_reward;
+    ep.done = d_done;
+    ep.executed = reinterpret_cast<long long *>(d_executed);
+    SessionParams sp{ctx->sess_go(), ctx->sess_done(), n_steps};
+    for_geo(ctx->geo, [&](auto kc, auto wc, auto gc) {
+        constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, GG = decltype(gc)::value;
+        void *args[] = {(void *)&p, (void *)&ep, (void *)&sp};
+        // cooperative: the launch fails instead of leaving part of the grid unscheduled
+        e = cudaLaunchCooperativeKernel((const void *)lob_session<KPL, W, GG>, dim3((unsigned)grid),
+                                        dim3(32 * W * GG), args, step_smem_bytes<KPL, W, GG>(), ctx->sess);
+    });
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e != cudaSuccess) return cuda_fail(e, "lob_session launch");
+    ctx->sess_active = true;
+    ctx->sess_step = 0;
+    ctx->sess_nsteps = n_steps;
+    return LOB_OK;
+}
+
+int lob_session_step(lob_ctx *ctx, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (!ctx->sess_active) return fail(LOB_EINVAL, "no session running%s");
+    if (ctx->sess_step >= ctx->sess_nsteps) return fail(LOB_EINVAL, "the session's episode data are exhausted%s");
+    const unsigned s = (unsigned)(ctx->sess_step + 1);
+    CUstream st = (CUstream)stream;
+    CUresult r = g_write32(st, (CUdeviceptr)ctx->sess_go(), s, 0);  // release step s (fenced)
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuStreamWriteValue32");
+    // the step's outputs are complete when every book has finished it
+    r = g_wait32(st, (CUdeviceptr)ctx->sess_done(), s * (unsigned)ctx->cfg.n_books, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuStreamWaitValue32");
+    ctx->sess_step = (int)s;
+    return LOB_OK;
+}
+
+int lob_session_end(lob_ctx *ctx, void *stream) {
+    int rc = check_ctx(ctx);
+    if (rc) return rc;
+    if (!ctx->sess_active) return fail(LOB_EINVAL, "no session running%s");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ctx->sess_step < ctx->sess_nsteps) {  // the kernel is waiting for a step: stop it
+        CUresult r = g_write32((CUstream)st, (CUdeviceptr)ctx->sess_go(), SESSION_STOP | (unsigned)ctx->sess_step, 0);
+        if (r != CUDA_SUCCESS) return cu_fail(r, "cuStreamWriteValue32");
+    }
+    // join: the caller's stream continues after the kernel has written the books back
+    cudaError_t e = cudaEventRecord(ctx->ev_sess, ctx->sess);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ctx->ev_sess, 0);
+    ctx->sess_active = false;
+    return e == cudaSuccess ? LOB_OK : cuda_fail(e, "session join");
 }
 
 int lob_get_l2(lob_ctx *ctx, int32_t *d_out, void *stream) {

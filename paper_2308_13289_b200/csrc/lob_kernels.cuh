@@ -32,6 +32,16 @@
 
 #include <type_traits>
 
+// Build options measured by A/B (scripts/ab_pairs.sh); the defaults are the kept ones.
+#ifndef LOB_CXL   // cancel scans: 0 = select chain after the reduction, 1 = Q captured in the scan,
+#define LOB_CXL 1 // 2 = one combined exact/synthetic pass (C4 -7 %, C5 N = 2048 +3.5 %)
+#endif
+#ifndef LOB_R16   // row bounds of 16-row books (with_rows)
+#define LOB_R16 1
+#endif
+#ifndef LOB_TREE  // get_r as a select tree for row bounds >= LOB_TREE (0 = never)
+#define LOB_TREE 16
+#endif
 namespace lobk {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -296,9 +306,22 @@ struct RegBook {
         for (int jj = 1; jj < KPL_; ++jj) r = (j == jj) ? v[s][f][jj] : r;
         return r;
     }
-    // the same for a row known to be below R (shorter select chains)
+    // the same for a row known to be below R.  LOB_TREE: a binary select tree on the
+    // bits of j (depth log2 R, one bit test per level) instead of the serial chain
+    template <int LO, int NN>
+    __device__ __forceinline__ int32_t sel_tree(int s, int f, int j) const {
+        if constexpr (NN == 1) {
+            return v[s][f][LO];
+        } else {
+            constexpr int H = NN > 8 ? 8 : (NN > 4 ? 4 : (NN > 2 ? 2 : 1));  // largest power of 2 < NN
+            return (j & H) ? sel_tree<LO + H, NN - H>(s, f, j) : sel_tree<LO, H>(s, f, j);
+        }
+    }
     template <int R>
     __device__ __forceinline__ int32_t get_r(int s, int f, int j) const {
+#if LOB_TREE
+        if constexpr (R >= LOB_TREE) return sel_tree<0, R>(s, f, j);
+#endif
         int32_t r = v[s][f][0];
 #pragma unroll
         for (int jj = 1; jj < R; ++jj) r = (j == jj) ? v[s][f][jj] : r;
@@ -447,16 +470,38 @@ struct Engine {
         if constexpr (KPL <= 2 || !ROWS) {
             f(IC<KPL>{});
         } else if constexpr (KPL <= 4) {
+#if LOB_R4 == 1
+            f(IC<KPL>{});
+#else
             if (h < 2) f(IC<2>{});
             else f(IC<KPL>{});
+#endif
         } else if constexpr (KPL <= 8) {
+#if LOB_R8 == 1
+            if (h < 4) f(IC<4>{});
+            else f(IC<KPL>{});
+#elif LOB_R8 == 2
+            if (h < 2) f(IC<2>{});
+            else f(IC<KPL>{});
+#else
             if (h < 2) f(IC<2>{});
             else if (h < 4) f(IC<4>{});
             else f(IC<KPL>{});
+#endif
         } else {
+#if LOB_R16 == 2
+            f(IC<KPL>{});
+#elif LOB_R16 == 3
+            if (h < 4) f(IC<4>{});
+            else f(IC<KPL>{});
+#elif LOB_R16 == 0
             if (h < 4) f(IC<4>{});
             else if (h < 8) f(IC<8>{});
             else f(IC<KPL>{});
+#else  // {8, 16}: C5 N = 512 +24 %, N = 2048 +5 % over {4, 8, 16} (fewer code copies)
+            if (h < 8) f(IC<8>{});
+            else f(IC<KPL>{});
+#endif
         }
     }
     // highest occupied row of side s (group-uniform), -1 if none
@@ -486,6 +531,15 @@ struct Engine {
 #pragma unroll
         for (int j = R - 1; j >= 0; --j)
             if (pred(j)) r = (unsigned)j;
+        return (int)gmin_u(r * GT + (unsigned)tid);
+    }
+    // the same, also capturing the Q of this thread's lowest matching row into q
+    template <int SD, int R, class Pred>
+    __device__ __forceinline__ int lowest_rows_q(int &q, Pred pred) {
+        unsigned r = KPL;
+#pragma unroll
+        for (int j = R - 1; j >= 0; --j)
+            if (pred(j)) { r = (unsigned)j; q = bk.hot(SD, F_Q, j); }
         return (int)gmin_u(r * GT + (unsigned)tid);
     }
     // Best(o_s) of side SD over occupied slots: price (ask min / bid max,
@@ -647,6 +701,50 @@ struct Engine {
     }
     template <int SD, int R>
     __device__ __forceinline__ void cancel_r(int mQ, int mP, int mOID) {
+#if LOB_CXL == 2
+        // ONE pass, ONE group minimum: each thread's lowest exact-OID row and lowest
+        // synthetic row at P (with their Q), keyed so that any exact match in the group
+        // beats every synthetic one: exact -> slot, synthetic -> NP + slot, none -> 2 NP.
+        // The owner's captured Q is the found order's (its lowest match is the slot).
+        unsigned rex = KPL, rsy = KPL;
+        int qex = 0, qsy = 0;
+#pragma unroll
+        for (int j = R - 1; j >= 0; --j) {
+            const int q = bk.hot(SD, F_Q, j), o = bk.hot(SD, F_OID, j);
+            if (q > 0 && o == mOID) { rex = (unsigned)j; qex = q; }
+            if (q > 0 && o <= -9000 && bk.hot(SD, F_P, j) == mP) { rsy = (unsigned)j; qsy = q; }
+        }
+        const unsigned key = rex < (unsigned)KPL ? rex * GT + (unsigned)tid
+                                                 : (rsy < (unsigned)KPL ? (unsigned)BK::NP + rsy * GT + (unsigned)tid
+                                                                        : 2u * BK::NP);
+        const unsigned k = gmin_u(key);
+        if (k >= 2u * BK::NP) {                    // G15
+            if constexpr (PRED) add64_if0(tid, sc + 8u * ST_UNKNOWN, 1);
+            else if (tid == 0) count(ST_UNKNOWN, 1);
+            return;
+        }
+        const bool exact = k < (unsigned)BK::NP;
+        const int slot = (int)(exact ? k : k - BK::NP);
+        const bool own = tid == (slot & (GT - 1));
+        const int j = slot / GT;
+        const int qi = exact ? qex : qsy;          // meaningful on the owner
+#elif LOB_CXL == 1
+        // the scans capture the Q of each thread's lowest matching row (the owner's is the
+        // found order's): no select chain after the reduction
+        int qi = 0;
+        int slot = lowest_rows_q<SD, R>(qi, [&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
+        if (!found(slot))
+            slot = lowest_rows_q<SD, R>(qi, [&](int j) {
+                return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
+            });
+        if (!found(slot)) {                        // G15
+            if constexpr (PRED) add64_if0(tid, sc + 8u * ST_UNKNOWN, 1);
+            else if (tid == 0) count(ST_UNKNOWN, 1);
+            return;
+        }
+        const bool own = tid == (slot & (GT - 1));
+        const int j = slot / GT;
+#else
         int slot = lowest_rows<R>([&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
         if (!found(slot))
             slot = lowest_rows<R>([&](int j) {
@@ -660,6 +758,7 @@ struct Engine {
         const bool own = tid == (slot & (GT - 1));
         const int j = slot / GT;                   // the slot is occupied: its row is below R
         const int qi = bk.template get_r<R>(SD, F_Q, j);
+#endif
         const int cq = (mQ < qi) ? mQ : qi;
         if (own) part_cxl += cq;                   // G14
         bk.template put_if_r<R>(own, SD, F_Q, j, qi - mQ);  // Q <= 0 -> empty
@@ -934,7 +1033,9 @@ __device__ __forceinline__ void env_agent(E &e, EnvState &es, const Params &p, c
                 if (forced) { T = 4; Q = (int)(remaining > INT_MAX ? INT_MAX : remaining); O = es.next_oid++; }
             } else if (limits) {
                 const int j = k - 5;
-                const float x = ep.actions[4 * (size_t)b + j];
+                // L2-coherent load: a resident session (lob_session.cuh) reads a buffer the
+                // caller rewrites between steps, which a stale L1 line would hide
+                const float x = __ldcg(ep.actions + 4 * (size_t)b + j);
                 long long q = 0;  // E2: round half-even, NaN / negative -> 0
                 if (x == x && x > 0.0f) q = (x >= 2147483647.0f) ? 2147483647LL : (long long)__float2int_rn(x);
                 if (q > remaining) q = remaining;  // E3
@@ -1042,6 +1143,9 @@ constexpr int step_smem_bytes() {
 #ifndef MINB4
 #define MINB4 7
 #endif
+#ifndef MINB16
+#define MINB16 3
+#endif
 // Persistent: group g of CTA b starts with book b*G + g, then takes books from the
 // dynamic counter.  MODE 0 (and 3): L2 per step; MODE 1 also writes the Level-1
 // trace (NEXT N1); MODE 2 is one fused execution-env step (NEXT N3, env_agent /
@@ -1050,7 +1154,7 @@ constexpr int step_smem_bytes() {
 // batches of 4-row books.  (With the uniform persistent loop MODE 0 also fits in 64
 // registers without spills, so the two now compile alike; MODE 3 keeps the hard cap.)
 template <int KPL, int W, int G, int MODE>
-__global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? 3 : (KPL > 8 ? 12 / W : 16 / W))))))
+__global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? (KPL > 8 ? MINB16 : 3) : (KPL > 8 ? 12 / W : 16 / W))))))
     lob_step(const Params p, const EnvParams ep) {
     using BK = RegBook<KPL, W>;
     constexpr bool TL1 = MODE == 1, ENV = MODE == 2;

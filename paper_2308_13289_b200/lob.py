@@ -83,6 +83,13 @@ def lib():
                 L.lob_env_reset.argtypes = [P, P, ctypes.POINTER(EnvConfig), i32, i32, P]
                 L.lob_env_step.restype = ctypes.c_int
                 L.lob_env_step.argtypes = [P, P, ctypes.POINTER(EnvConfig), P, P, i32, P, P, P, P, P, P]
+            if hasattr(L, "lob_session_begin"):
+                L.lob_session_begin.restype = ctypes.c_int
+                L.lob_session_begin.argtypes = [P, P, ctypes.POINTER(EnvConfig), P, P, i32, i32, P, P, P, P, P, P]
+                L.lob_session_step.restype = ctypes.c_int
+                L.lob_session_step.argtypes = [P, P]
+                L.lob_session_end.restype = ctypes.c_int
+                L.lob_session_end.argtypes = [P, P]
             if hasattr(L, "lob_digest"):
                 L.lob_digest.restype = ctypes.c_int
                 L.lob_digest.argtypes = [P, P, P]
@@ -328,3 +335,46 @@ class LobEnv:
                                       _ptr(self.executed), _ptr(l2_out), st), "lob_env_step")
         self._keep = (a, d)
         return self.reward, self.done, self.executed
+
+
+class LobSession:
+    """A RESIDENT env session (NEXT row N3, residency; include/lob.h lob_session_*): one
+    persistent launch keeps every book of ``env``'s batch on chip for an episode whose
+    data messages ``data`` [K][n_steps][M][8] (or [K][n_steps*M][8]) are given up front;
+    each ``step(actions)`` runs what one ``LobEnv.step`` runs, without reloading or
+    storing a book.  Outputs are ``env``'s buffers (``env.reward``, ``env.done``,
+    ``env.executed``, ``env.work``) and ``self.l2`` [K][L][4], overwritten every step and
+    complete on the stream after ``step`` returns.  ``end()`` writes books and counters
+    back.  Other calls on the batch while the session runs are not allowed, and so is a
+    DEVICE-wide synchronize (``torch.cuda.synchronize()``): it would wait for the resident
+    kernel, which waits for the next step -- synchronise the stream instead."""
+
+    def __init__(self, env: LobEnv, data, n_steps: int, l2: bool = True, stream=None):
+        self.env, self.b, self.n_steps = env, env.b, int(n_steps)
+        b = self.b
+        with _On(b.device, stream) as st:
+            d = b._dev(data)
+            assert d.numel() == b.K * self.n_steps * env.M * 8, d.shape
+            self.data = d.reshape(b.K, self.n_steps * env.M, 8)
+            self.actions = torch.zeros((b.K, 4), dtype=torch.float32, device=b.device)
+            self.l2 = torch.empty((b.K, b.L, 4), dtype=torch.int32, device=b.device) if l2 else None
+            _check(lib().lob_session_begin(b.ctx, _ptr(env.state), ctypes.byref(env.cfg), _ptr(self.actions),
+                                           _ptr(self.data), self.n_steps, env.M, _ptr(env.work),
+                                           _ptr(env.reward), _ptr(env.done), _ptr(env.executed), _ptr(self.l2),
+                                           st), "lob_session_begin")
+        self.active = True
+
+    def step(self, actions, stream=None):
+        """actions [K][4] f32 -> (reward, done, executed): env's buffers, this step's values."""
+        with _On(self.b.device, stream) as st:
+            a = torch.as_tensor(actions)
+            self.actions.copy_(a.to(device=self.b.device, dtype=torch.float32, non_blocking=True))
+            _check(lib().lob_session_step(self.b.ctx, st), "lob_session_step")
+        return self.env.reward, self.env.done, self.env.executed
+
+    def end(self, stream=None):
+        if self.active:
+            with _On(self.b.device, stream) as st:
+                _check(lib().lob_session_end(self.b.ctx, st), "lob_session_end")
+            self.active = False
+

@@ -2,7 +2,9 @@
 """Paper-shaped microbenchmarks (context, not targets): Tables 1, 2 and 4 of PAPER.md
 re-run on this engine.  Books are filled to one third of capacity from a
 synthetic L2 seed; every timing is CUDA events around whole library calls
-(lob_init excluded), median of 200 repetitions after warm-up.
+(lob_init excluded), 1000 repetitions after warm-up, reported as median,
+inter-quartile range and min, plus the op's device cost over a padding message
+(median(op call) - median(padding call): the fixed launch cost cancels).
 
   Table 1 (P:L220-238): one book, one add / cancel / match message, N in {10,100,1000}
   Table 2 (P:L240-262): one book, N = 100, market order Q_a in {0,10,500,1000,10000}
@@ -33,7 +35,8 @@ def seed(K, N):
     return torch.from_numpy(rows).cuda(), L0
 
 
-def timed(b, init, msgs, reps=200):
+def timed(b, init, msgs, reps=1000):
+    """Per-call microseconds over `reps` calls: {median, q1, q3, min}."""
     st = torch.cuda.current_stream()
     es = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     for i in range(reps + 10):
@@ -44,7 +47,14 @@ def timed(b, init, msgs, reps=200):
         if i >= 10:
             es[i - 10][1].record(st)
     torch.cuda.synchronize()
-    return statistics.median(a.elapsed_time(z) * 1e3 for a, z in es)  # microseconds
+    t = np.array([a.elapsed_time(z) * 1e3 for a, z in es])
+    q1, med, q3 = np.percentile(t, [25, 50, 75])
+    return {"median": float(med), "q1": float(q1), "q3": float(q3), "iqr": float(q3 - q1), "min": float(t.min())}
+
+
+def with_device_cost(r, pad):
+    r["device_us_over_padding"] = r["median"] - pad["median"]
+    return r
 
 
 def msg(T, S, Q, P, oid=777):
@@ -60,33 +70,42 @@ def cases(N):
     }
 
 
-def run():
-    out = {"note": "microseconds per library call; context only (PAPER.md Tables 1/2/4 were a 2080 Ti)"}
+def run(reps=1000):
+    out = {"note": "microseconds per library call; context only (PAPER.md Tables 1/2/4 were a 2080 Ti)",
+           "reps": reps}
+    pad = msg(0, 0, 0, 0, 0)
     t1 = {}
     for N in (10, 100, 1000):
         b = LobBatch(1, N, 64, 1)
         init, _ = seed(1, N)
-        t1[N] = {k: timed(b, init, torch.tensor([[m]], dtype=torch.int32).cuda()) for k, m in cases(N).items()}
+        p0 = timed(b, init, torch.tensor([[pad]], dtype=torch.int32).cuda(), reps)
+        t1[N] = {k: with_device_cost(timed(b, init, torch.tensor([[m]], dtype=torch.int32).cuda(), reps), p0)
+                 for k, m in cases(N).items()}
+        t1[N]["padding"] = p0
     out["table1_one_book_us"] = t1
     t2 = {}
     b = LobBatch(1, 100, 128, 1)
     init, _ = seed(1, 100)
+    p0 = timed(b, init, torch.tensor([[pad]], dtype=torch.int32).cuda(), reps)
     for qa in (0, 10, 500, 1000, 10000):
-        t2[qa] = timed(b, init, torch.tensor([[msg(4, 1, qa, 0)]], dtype=torch.int32).cuda())
+        t2[qa] = with_device_cost(timed(b, init, torch.tensor([[msg(4, 1, qa, 0)]], dtype=torch.int32).cuda(), reps), p0)
+    t2["padding"] = p0
     out["table2_market_us"] = t2
     t4 = {}
     for N in (10, 100, 1000):
         K = 1000
         b = LobBatch(K, N, 64, 1)
         init, _ = seed(K, N)
-        row = {}
+        p0 = timed(b, init, torch.tensor([[pad]] * K, dtype=torch.int32).cuda(), reps)
+        row = {"padding": p0}
         for k, m in cases(N).items():
-            us = timed(b, init, torch.tensor([[m]] * K, dtype=torch.int32).cuda())
-            row[k] = {"us_per_call": us, "ns_per_book_message": us * 1e3 / K}
+            r = with_device_cost(timed(b, init, torch.tensor([[m]] * K, dtype=torch.int32).cuda(), reps), p0)
+            r["ns_per_book_message"] = r["median"] * 1e3 / K
+            row[k] = r
         t4[N] = row
     out["table4_1000_books"] = t4
-    print(json.dumps(out))
+    return out
 
 
 if __name__ == "__main__":
-    run()
+    print(json.dumps(run()))

@@ -90,7 +90,7 @@ def test_product_path_never_touches_the_oracle():
 
 def test_step_kernels_are_warp_uniform():
     """Performance guard ("uniform persistent loop"): the one-warp
-    step kernels (plain, L1-trace, many-wave and fused env step) must compile with the persistent loop proven warp-uniform -- no
+    step kernels (plain, L1-trace, many-wave, fused env step, resident session) must compile with the persistent loop proven warp-uniform -- no
     divergence checks (BRA.DIV) before warp collectives.  ptxas's convergence proof is
     fragile (an unrelated source edit once cost C4 15 % through ~17 extra control
     instructions per message), so the SASS is checked here, without a GPU."""
@@ -99,18 +99,20 @@ def test_step_kernels_are_warp_uniform():
     funcs = re.split(r"\n\s*Function : ", sass)
     checked = 0
     for f in funcs:
-        m = re.match(r"_ZN4lobk8lob_stepILi(\d+)ELi1ELi4ELi([0-3])E", f)
+        m = re.match(r"_ZN4lobk8lob_stepILi(\d+)ELi1ELi4ELi([0-3])E", f) or \
+            re.match(r"_ZN4lobk11lob_sessionILi(\d+)ELi1ELi4E()", f)
         if not m:
             continue
         checked += 1
         n_div = f.count("BRA.DIV")
-        assert n_div == 0, f"lob_step<KPL={m.group(1)}, W=1, MODE={m.group(2)}> has {n_div} BRA.DIV"
-    assert checked >= 19, checked  # MODE 0 (step), 1 (L1 trace), 2 (fused env step), 3 (many-wave step)
+        assert n_div == 0, f"{f[:40]} (KPL={m.group(1)}, W=1, MODE={m.group(2)}) has {n_div} BRA.DIV"
+    # MODE 0 (step), 1 (L1 trace), 2 (fused env step), 3 (many-wave step), resident session
+    assert checked >= 25, checked
 
 
 def test_bench_kernel_register_budget():
     """Performance guard: the C4 bench kernel (lob_step<4,1,4,3>, 8 CTAs/SM) must fit in
-    64 registers with at most a small per-book spill (44 bytes since v23: the book-load
+    64 registers with exactly the known per-book spill (44 bytes since v23: the book-load
     prologue, executed once per book, never in the message loop -- DESIGN.md section 7,
     "Occupancy").  Reads the ptxas report `make` writes next to the library; skipped
     when the library was built elsewhere."""
@@ -124,6 +126,6 @@ def test_bench_kernel_register_budget():
             m = re.search(r"Used (\d+) registers", block)
             s = re.search(r"(\d+) bytes spill stores", block)
             assert m and int(m.group(1)) <= 64, block
-            assert s and int(s.group(1)) <= 64, block
+            assert s and int(s.group(1)) == 44, block  # pinned: any change must be looked at
             return
     pytest.skip("bench kernel not in ptxas.log")
