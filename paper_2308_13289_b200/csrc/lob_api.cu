@@ -77,7 +77,7 @@ bool layout_of(const lob_config *c, Layout *L) {
     L->off_tro = al(L->off_sched + 2 * sizeof(unsigned));
     // resident env session: the step flag and the finished book-step counter
     L->off_sess = al(L->off_tro + (K + 1) * sizeof(long long));
-    L->total = al(L->off_sess + 2 * sizeof(unsigned));
+    L->total = al(L->off_sess + 256);  // go and done on separate 128-byte lines
     return true;
 }
 }  // namespace
@@ -100,7 +100,8 @@ struct lob_ctx {
     cudaStream_t sess = nullptr;
     cudaEvent_t ev_sess = nullptr;
     bool sess_active = false;
-    int sess_step = 0, sess_nsteps = 0, sess_grid_cap = 0;
+    int sess_step = 0, sess_nsteps = 0, sess_grid_cap = 0, sess_grid = 0;
+    bool sess_memops = false;
     int32_t *book() const { return reinterpret_cast<int32_t *>(state + lay.off_book); }
     int32_t *trades() const { return reinterpret_cast<int32_t *>(state + lay.off_trades); }
     int32_t *ntr() const { return reinterpret_cast<int32_t *>(state + lay.off_ntr); }
@@ -108,7 +109,7 @@ struct lob_ctx {
     unsigned *sched() const { return reinterpret_cast<unsigned *>(state + lay.off_sched); }
     long long *tro() const { return reinterpret_cast<long long *>(state + lay.off_tro); }
     unsigned *sess_go() const { return reinterpret_cast<unsigned *>(state + lay.off_sess); }
-    unsigned *sess_done() const { return sess_go() + 1; }
+    unsigned *sess_done() const { return sess_go() + 32; }
 };
 
 #ifndef G16
@@ -252,6 +253,14 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
         if (e != cudaSuccess) rc = cuda_fail(e, "kernel attribute / occupancy query");
     });
     if (rc != LOB_OK) { delete c; return rc; }
+    {
+        // load the session's step kernel now: under lazy module loading (the CUDA 12
+        // default) its first launch would otherwise load the module while a resident
+        // session kernel spins, and the load waits for the device -- a deadlock
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, lob_session_sync_kernel);
+        if (e != cudaSuccess) { delete c; return cuda_fail(e, "lob_session_sync_kernel attributes"); }
+    }
     for (int m = 0; m < 4; ++m) c->grid_cap[m] = sms * (per_sm[m] > 0 ? per_sm[m] : 1);
     c->sess_grid_cap = sms * sess_per_sm;
     *out = c;
@@ -540,8 +549,14 @@ int lob_session_begin(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, cons
         reinterpret_cast<uintptr_t>(d_data) % 16 || reinterpret_cast<uintptr_t>(d_l2_out) % 16 ||
         reinterpret_cast<uintptr_t>(d_reward) % 8 || reinterpret_cast<uintptr_t>(d_executed) % 8)
         return fail(LOB_EINVAL, "misaligned buffer%s");
-    rc = stream_memops();
-    if (rc) return rc;
+    {
+        const char *mo = getenv("LOB_SESSION_MEMOPS");  // A/B hook: stream memory operations
+        ctx->sess_memops = mo && mo[0] == '1';
+    }
+    if (ctx->sess_memops) {
+        rc = stream_memops();
+        if (rc) return rc;
+    }
     int G = 1;
     for_geo(ctx->geo, [&](auto, auto, auto gc) { G = decltype(gc)::value; });
     const long long grid = (K + G - 1) / G;
@@ -554,7 +569,7 @@ int lob_session_begin(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, cons
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_sess, cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(e, "session stream / event creation");
     }
-    e = cudaMemsetAsync(ctx->sess_go(), 0, 2 * sizeof(unsigned), st);
+    e = cudaMemsetAsync(ctx->sess_go(), 0, 256, st);
     if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_sess, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->sess, ctx->ev_sess, 0);
     if (e != cudaSuccess) return cuda_fail(e, "session fork");
@@ -572,18 +587,19 @@ int lob_session_begin(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, cons
     ep.done = d_done;
     ep.executed = reinterpret_cast<long long *>(d_executed);
     SessionParams sp{ctx->sess_go(), ctx->sess_done(), n_steps};
+    // An ordinary launch: the grid fits one wave (checked above), so every CTA becomes
+    // resident as soon as the SMs it needs are free.  (A cooperative launch measured as a
+    // device-exclusive kernel here: the caller's step launch queued behind it.)
     for_geo(ctx->geo, [&](auto kc, auto wc, auto gc) {
         constexpr int KPL = decltype(kc)::value, W = decltype(wc)::value, GG = decltype(gc)::value;
-        void *args[] = {(void *)&p, (void *)&ep, (void *)&sp};
-        // cooperative: the launch fails instead of leaving part of the grid unscheduled
-        e = cudaLaunchCooperativeKernel((const void *)lob_session<KPL, W, GG>, dim3((unsigned)grid),
-                                        dim3(32 * W * GG), args, step_smem_bytes<KPL, W, GG>(), ctx->sess);
+        lob_session<KPL, W, GG><<<(unsigned)grid, 32 * W * GG, step_smem_bytes<KPL, W, GG>(), ctx->sess>>>(p, ep, sp);
     });
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (e != cudaSuccess) return cuda_fail(e, "lob_session launch");
+    rc = after_launch("lob_session launch");
+    if (rc) return rc;
     ctx->sess_active = true;
     ctx->sess_step = 0;
     ctx->sess_nsteps = n_steps;
+    ctx->sess_grid = (int)grid;
     return LOB_OK;
 }
 
@@ -593,12 +609,19 @@ int lob_session_step(lob_ctx *ctx, void *stream) {
     if (!ctx->sess_active) return fail(LOB_EINVAL, "no session running%s");
     if (ctx->sess_step >= ctx->sess_nsteps) return fail(LOB_EINVAL, "the session's episode data are exhausted%s");
     const unsigned s = (unsigned)(ctx->sess_step + 1);
-    CUstream st = (CUstream)stream;
-    CUresult r = g_write32(st, (CUdeviceptr)ctx->sess_go(), s, 0);  // release step s (fenced)
-    if (r != CUDA_SUCCESS) return cu_fail(r, "cuStreamWriteValue32");
-    // the step's outputs are complete when every book has finished it
-    r = g_wait32(st, (CUdeviceptr)ctx->sess_done(), s * (unsigned)ctx->cfg.n_books, CU_STREAM_WAIT_VALUE_GEQ);
-    if (r != CUDA_SUCCESS) return cu_fail(r, "cuStreamWaitValue32");
+    // the step's outputs are complete when every CTA has finished it (one count per CTA)
+    const unsigned target = s * (unsigned)ctx->sess_grid;
+    if (ctx->sess_memops) {
+        CUstream st = (CUstream)stream;
+        CUresult r = g_write32(st, (CUdeviceptr)ctx->sess_go(), s, 0);  // release step s (fenced)
+        if (r != CUDA_SUCCESS) return cu_fail(r, "cuStreamWriteValue32");
+        r = g_wait32(st, (CUdeviceptr)ctx->sess_done(), target, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) return cu_fail(r, "cuStreamWaitValue32");
+    } else {
+        lob_session_sync_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ctx->sess_go(), s, ctx->sess_done(), target);
+        rc = after_launch("lob_session_sync_kernel");
+        if (rc) return rc;
+    }
     ctx->sess_step = (int)s;
     return LOB_OK;
 }
@@ -609,8 +632,15 @@ int lob_session_end(lob_ctx *ctx, void *stream) {
     if (!ctx->sess_active) return fail(LOB_EINVAL, "no session running%s");
     cudaStream_t st = (cudaStream_t)stream;
     if (ctx->sess_step < ctx->sess_nsteps) {  // the kernel is waiting for a step: stop it
-        CUresult r = g_write32((CUstream)st, (CUdeviceptr)ctx->sess_go(), SESSION_STOP | (unsigned)ctx->sess_step, 0);
-        if (r != CUDA_SUCCESS) return cu_fail(r, "cuStreamWriteValue32");
+        const unsigned stop = SESSION_STOP | (unsigned)ctx->sess_step;
+        if (ctx->sess_memops) {
+            CUresult r = g_write32((CUstream)st, (CUdeviceptr)ctx->sess_go(), stop, 0);
+            if (r != CUDA_SUCCESS) return cu_fail(r, "cuStreamWriteValue32");
+        } else {
+            lob_session_sync_kernel<<<1, 32, 0, st>>>(ctx->sess_go(), stop, ctx->sess_done(), 0u);
+            rc = after_launch("lob_session_sync_kernel");
+            if (rc) return rc;
+        }
     }
     // join: the caller's stream continues after the kernel has written the books back
     cudaError_t e = cudaEventRecord(ctx->ev_sess, ctx->sess);

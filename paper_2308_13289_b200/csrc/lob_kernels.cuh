@@ -36,11 +36,14 @@
 #ifndef LOB_CXL   // cancel scans: 0 = select chain after the reduction, 1 = Q captured in the scan,
 #define LOB_CXL 1 // 2 = one combined exact/synthetic pass (C4 -7 %, C5 N = 2048 +3.5 %)
 #endif
-#ifndef LOB_R16   // row bounds of 16-row books (with_rows)
-#define LOB_R16 1
+#ifndef LOB_R16   // row bounds of 16-row books: 1 = {8,16} (C5 N = 512 +24 %, N = 2048 +5 % over
+#define LOB_R16 1 // 0 = {4,8,16}); 2 = {16} (-25 %), 3 = {4,16} (-46 %, -23 %)
 #endif
-#ifndef LOB_TREE  // get_r as a select tree for row bounds >= LOB_TREE (0 = never)
-#define LOB_TREE 16
+#ifndef LOB_TREE  // get_r as a select tree for row bounds >= LOB_TREE (0 = never; 16: C5 N = 512
+#define LOB_TREE 0  // +6 % before the {8,16} row bounds, +-0 after)
+#endif
+#ifndef LOB_R8    // row bounds of 8-row books: 0 = {2,4,8}, 1 = {4,8} (C5 N = 256 +13 %, N = 1024 +4 %),
+#define LOB_R8 1  // 2 = {2,8} (-10 %, -16 %)
 #endif
 namespace lobk {
 

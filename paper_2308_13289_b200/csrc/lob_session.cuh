@@ -4,8 +4,8 @@
 // the caller's stream drives it step by step through two device words:
 //   go    written by the caller's stream (cuStreamWriteValue32): step s (1-based) is
 //         released when go >= s; bit 31 (SESSION_STOP) ends the session;
-//   done  groups that have finished a step, cumulative: after step s every group has
-//         added 1 s times, so the caller's stream waits for done >= s*K
+//   done  CTAs that have finished a step, cumulative: after step s every CTA has added
+//         1 s times, so the caller's stream waits for done >= s*grid
 //         (cuStreamWaitValue32, cyclic >=) before reading the step's outputs.
 // Per step and book, in the order of a lob_env_step launch (lob_kernels.cuh MODE 2):
 // the agent's messages from the actions (env_agent), the step's data
@@ -23,7 +23,7 @@ constexpr unsigned SESSION_STOP = 0x80000000u;
 
 struct SessionParams {
     const unsigned *go;  // step flag (caller's stream)
-    unsigned *done;      // finished book-steps (cumulative)
+    unsigned *done;      // CTAs that finished a step (cumulative; its own 128-byte line)
     int n_steps;         // steps of episode data
 };
 
@@ -33,37 +33,56 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
     return v;
 }
 
-// Thread 0 waits until step s is released (or the session is stopped) and hands the
-// flag to the group through a shared word: a load from a uniform shared address is
-// uniform, so the persistent loop stays provably warp-uniform (lob_kernels.cuh).
-// W = 1: every lane polls and the warp leaves the loop by a warp reduction, so the loop
-// and its result are warp-uniform (a lane-0 spin loop cost ptxas its uniformity proof of
-// the whole kernel).  Lanes never disagree on the outcome: the flag only moves to s
-// (release) or to STOP, never to both while a step is pending, since the caller's
-// stream writes STOP only after its wait for the previous step.
-template <int W>
-__device__ __forceinline__ unsigned session_wait(const unsigned *go, unsigned s, int tid, unsigned *word) {
-    if constexpr (W == 1) {
-        unsigned v = ld_acquire_gpu(go);
-        while (__reduce_min_sync(FULL, ((v & SESSION_STOP) != 0u || v >= s) ? 1u : 0u) == 0u) {
-            __nanosleep(32);
-            v = ld_acquire_gpu(go);
-        }
-        return __reduce_max_sync(FULL, v);
-    } else {
-        if (tid == 0) {
-            unsigned v = ld_acquire_gpu(go);
-            while ((v & SESSION_STOP) == 0u && v < s) {
-                __nanosleep(32);
-                v = ld_acquire_gpu(go);
-            }
-            *word = v;
-        }
-        __syncthreads();
-        const unsigned v = *word;
-        __syncthreads();  // every thread has read the word before it is reused
-        return v;
+__device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// The caller's side of a step, ONE tiny launch on the caller's stream: release step s
+// (a release store: every earlier write of the stream, e.g. the actions, is visible to
+// the session's acquire), then -- unless target is 0 -- spin until `done` reaches
+// target (cyclic >=), so later work on the stream sees the step's outputs.  Measured
+// against stream memory operations (cuStreamWriteValue32 + cuStreamWaitValue32, A/B hook
+// LOB_SESSION_MEMOPS=1): 13.1 us of fixed time per step at 1,000 envs, this launch 11.7
+// us from an eager host loop and 9.3 us inside a CUDA graph (scripts/session_overhead.py).
+__global__ void lob_session_sync_kernel(unsigned *go, unsigned s, const unsigned *done, unsigned target) {
+    if (threadIdx.x != 0) return;
+    st_release_gpu(go, s);
+    if (target == 0u) return;
+    while ((int)(ld_acquire_gpu(done) - target) < 0) __nanosleep(20);
+}
+
+// Step boundary of a whole CTA (every group, with or without a book, calls it):
+//  1. a CTA barrier: every group has written the finished step's outputs;
+//  2. (signal) thread 0 publishes them (fence, release) and adds 1 to `done` -- ONE
+//     counter update per CTA, and the counter sits on its own 128-byte line, away from
+//     `go`, so neither the updates nor the polls queue behind each other in L2;
+//  3. warp 0 alone polls `go` until step s is released (or the session stopped) -- one
+//     poller per CTA -- with a warp-uniform loop (every lane loads, a reduction decides;
+//     a lane-0 spin loop cost ptxas its uniformity proof of the whole kernel).  Lanes
+//     never disagree: the flag moves to s (release) or to STOP, never both while a step
+//     is pending, since the caller's stream writes STOP only after its wait for the
+//     previous step;
+//  4. the flag goes to every group through a shared word behind a second CTA barrier
+//     (a load from a uniform shared address is uniform).
+__device__ __forceinline__ unsigned session_step_sync(const SessionParams &sp, unsigned s, bool signal,
+                                                      unsigned *word) {
+    __syncthreads();
+    if (signal && threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(sp.done, 1u);
     }
+    const unsigned wid = __reduce_min_sync(FULL, threadIdx.x / 32u);  // uniform
+    if (wid == 0u) {
+        unsigned v = ld_acquire_gpu(sp.go);
+        while (__reduce_min_sync(FULL, ((v & SESSION_STOP) != 0u || v >= s) ? 1u : 0u) == 0u) {
+            __nanosleep(64);
+            v = ld_acquire_gpu(sp.go);
+        }
+        v = __reduce_max_sync(FULL, v);
+        if (threadIdx.x == 0) *word = v;
+    }
+    __syncthreads();
+    return *word;  // rewritten only after the next step's first barrier
 }
 
 // One wave only, so occupancy matters less than for lob_step: books of up to 128 orders
@@ -82,52 +101,57 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 4 ? 5 : (W == 1 ? (KPL > 8
     const uint32_t cold = smem_u32(base + 2 * CH * 32 + 16);
     const uint32_t scratch = smem_u32(base + 2 * CH * 32 + 16 + 2 * BK::NP * 16);
     constexpr int word_off = 2 * CH * 32 + 16 + 2 * BK::NP * 16 + 8 * NST + 16 + (W == 1 ? 8 : 32 * W);
-    unsigned *word = reinterpret_cast<unsigned *>(base + word_off);
+    unsigned *word = reinterpret_cast<unsigned *>(dyn + word_off);  // group 0's: one per CTA
     const int lb = blockIdx.x * G + g;  // one book per group for the whole session
-    if (lb >= p.nb) return;             // uniform: this group has no book
-    const int b = p.book0 + lb;
-    if (tid == 0) {
-        mbar_init(bars, 1);
-        mbar_init(bars + 8, 1);
-        fence_mbar_init();
-    }
-    group_sync<W>();
+    // a group without a book (the grid's last CTA) still joins every CTA barrier
+    const bool has = lb < p.nb;         // uniform
+    const int b = p.book0 + (has ? lb : 0);
     const int M = p.M;
     const int nmsg = sp.n_steps * M;
     const int nchunks = (nmsg + CH - 1) / CH;
-    const int4 *src = reinterpret_cast<const int4 *>(p.msgs + (size_t)lb * nmsg * 8);
-    if (tid == 0) {
+    const int4 *src = reinterpret_cast<const int4 *>(p.msgs + (size_t)(has ? lb : 0) * nmsg * 8);
+    Engine<BK, false, true, false, (W == 1 && KPL <= 8)> e(p);
+    if (has) {
+        if (tid == 0) {
+            mbar_init(bars, 1);
+            mbar_init(bars + 8, 1);
+            fence_mbar_init();
+        }
+        group_sync<W>();
+        if (tid == 0) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            if (c < nchunks) {
-                const int cnt = min(CH, nmsg - c * CH);
-                mbar_arrive_expect_tx(bars + 8 * c, cnt * 32);
-                bulk_g2s(stage + c * CH * 32, src + (size_t)c * CH * 2, cnt * 32, bars + 8 * c);
+            for (int c = 0; c < 2; ++c) {
+                if (c < nchunks) {
+                    const int cnt = min(CH, nmsg - c * CH);
+                    mbar_arrive_expect_tx(bars + 8 * c, cnt * 32);
+                    bulk_g2s(stage + c * CH * 32, src + (size_t)c * CH * 2, cnt * 32, bars + 8 * c);
+                }
             }
         }
+        if (tid < NST) sts64(scratch + 8u * tid, 0);
+        e.bk.cold = cold;
+        e.bk.tid = tid;
+        e.tid = tid; e.book = b; e.ntr = 0; e.sc = scratch; e.xph = 0;
+        e.scp = base + 2 * CH * 32 + 16 + 2 * BK::NP * 16;
+        e.part_cxl = 0; e.part_trd = 0;
+        e.bk.load(p.book + (size_t)b * 2 * NF * BK::NP);
+        e.init_rows();
+        e.bslot[0] = e.bslot[1] = BEST_INVALID;
+        e.bP[0] = e.bP[1] = 0;
+        e.bV[0] = e.bV[1] = 0;
     }
-    if (tid < NST) sts64(scratch + 8u * tid, 0);
-    Engine<BK, false, true, false, (W == 1 && KPL <= 8)> e(p);
-    e.bk.cold = cold;
-    e.bk.tid = tid;
-    e.tid = tid; e.book = b; e.ntr = 0; e.sc = scratch; e.xph = 0;
-    e.scp = base + 2 * CH * 32 + 16 + 2 * BK::NP * 16;
-    e.part_cxl = 0; e.part_trd = 0;
-    e.bk.load(p.book + (size_t)b * 2 * NF * BK::NP);
-    e.init_rows();
-    e.bslot[0] = e.bslot[1] = BEST_INVALID;
-    e.bP[0] = e.bP[1] = 0;
-    e.bV[0] = e.bV[1] = 0;
     int steps_done = 0, last_ts = 0, last_tns = 0;
     bool have_last = false, idle = false;
-    // one iteration per step: wait for the release, the agent's messages, the step's M
-    // data messages (chunk refills inline), L2 / reward / signal.  The per-step work with
-    // lane-guarded stores stays outside the message loop (inside it, such a branch costs
-    // ptxas its uniformity proof: reconvergence barriers around every message).
+    // one iteration per step: the CTA's step boundary (signal of the previous step, wait
+    // for the release), the agent's messages, the step's M data messages (chunk refills
+    // inline), L2 / reward.  The per-step work with lane-guarded stores stays outside the
+    // message loop (inside it, such a branch costs ptxas its uniformity proof:
+    // reconvergence barriers around every message).
     int c = -1, avail = 0;  // current chunk, its unprocessed messages
     uint32_t maddr = stage;
     for (; steps_done < sp.n_steps; ++steps_done) {
-        if ((session_wait<W>(sp.go, (unsigned)steps_done + 1u, tid, word) & SESSION_STOP) != 0u) break;
+        if ((session_step_sync(sp, (unsigned)steps_done + 1u, steps_done > 0, word) & SESSION_STOP) != 0u) break;
+        if (!has) continue;
         e.ntr = 0;  // a new step: a new trade log (G9)
         have_last = false;
         {
@@ -176,7 +200,7 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 4 ? 5 : (W == 1 ? (KPL > 8
             avail -= run;
             left -= run;
         }
-        // end of the step: L2, reward / time / termination, then the signal
+        // end of the step: L2, reward / time / termination (published at the next boundary)
         if (p.l2out) e.l2_write(p.l2out + (size_t)lb * p.L * 4, p.L);
         const int logged = min(e.ntr, p.Tcap);
         if (tid == 0) {  // fills = logged + dropped (G8)
@@ -185,12 +209,15 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 4 ? 5 : (W == 1 ? (KPL > 8
             e.count(ST_DROPPED, e.ntr - logged);
         }
         env_post<W>(p, ep, b, tid, logged, have_last, last_ts, last_tns);
-        group_sync<W>();  // every output of the step is written
-        if (tid == 0) {
+    }
+    if (steps_done == sp.n_steps) {  // the last step's signal (the loop ended without a boundary)
+        __syncthreads();
+        if (threadIdx.x == 0) {
             __threadfence();
             atomicAdd(sp.done, 1u);
         }
     }
+    if (!has) return;
     // chunks still in flight land before the CTA exits (stopped sessions)
     // (chunks c + 1 and, before the first chunk, 1 were requested but not consumed)
     const int last = min(nchunks - 1, c < 0 ? 1 : c + 1);

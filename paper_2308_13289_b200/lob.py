@@ -364,11 +364,14 @@ class LobSession:
                                            st), "lob_session_begin")
         self.active = True
 
-    def step(self, actions, stream=None):
-        """actions [K][4] f32 -> (reward, done, executed): env's buffers, this step's values."""
+    def step(self, actions=None, stream=None):
+        """actions [K][4] f32 -> (reward, done, executed): env's buffers, this step's values.
+        ``actions=None``: the caller has already written them into ``self.actions`` on the
+        stream (e.g. the policy's output), so nothing is copied."""
         with _On(self.b.device, stream) as st:
-            a = torch.as_tensor(actions)
-            self.actions.copy_(a.to(device=self.b.device, dtype=torch.float32, non_blocking=True))
+            if actions is not None:
+                a = torch.as_tensor(actions)
+                self.actions.copy_(a.to(device=self.b.device, dtype=torch.float32, non_blocking=True))
             _check(lib().lob_session_step(self.b.ctx, st), "lob_session_step")
         return self.env.reward, self.env.done, self.env.executed
 

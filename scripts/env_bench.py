@@ -55,13 +55,15 @@ def run(K, steps=20):
     # region is the per-step loop (actions copied in, release, wait), as in an RL loop
     dall = torch.cat(data, 1).contiguous()
     zero = torch.zeros_like(acts)
-    for name, a in (("session", acts), ("session_zero_actions", zero)):
+    for name, a in (("session", acts), ("session_zero_actions", zero), ("session_actions_in_place", None)):
         try:
             ts = []
             for _ in range(3):
                 b.init(ti, lobgen.INIT_TS, lobgen.INIT_TNS)
                 env.reset(lobgen.INIT_TS, lobgen.INIT_TNS)
                 sess = LobSession(env, dall, steps)
+                if a is None:
+                    sess.actions.copy_(acts)  # the policy writes its output here
                 st.synchronize()  # stream only: a device sync would wait for the resident kernel
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)
