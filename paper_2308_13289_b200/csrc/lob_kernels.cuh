@@ -33,9 +33,9 @@
 #include <type_traits>
 
 // Build options measured by A/B (scripts/ab_pairs.sh); the defaults are the kept ones.
-#ifndef LOB_CXL   // cancel scans: 0 = select chain after the reduction, 1 = Q captured in the scan,
-#define LOB_CXL 1 // 2 = one combined exact/synthetic pass (C4 -7 %, C5 N = 2048 +3.5 %)
-#endif
+#ifndef LOB_CXL2_W    // books of >= this many warps cancel in ONE combined exact / synthetic
+#define LOB_CXL2_W 2    // pass (C5 N = 1024 / 2048 +1.4 %; one-warp books: C4 -7 %, C2 -4.5 %,
+#endif                  // C5 N = 256 / 512 -1 %)
 #ifndef LOB_R16   // row bounds of 16-row books: 1 = {8,16} (C5 N = 512 +24 %, N = 2048 +5 % over
 #define LOB_R16 1 // 0 = {4,8,16}); 2 = {16} (-25 %), 3 = {4,16} (-46 %, -23 %)
 #endif
@@ -702,57 +702,45 @@ struct Engine {
         // one row-bound branch for the whole cancel: scans and owner update over R rows
         with_rows(hr[SD], [&](auto R) { cancel_r<SD, R>(mQ, mP, mOID); });
     }
+    // the cancelled order: its slot (or none, >= NP) and, on the owner thread, its Q
+    template <int SD, int R>
+    __device__ __forceinline__ int cancel_find(int mP, int mOID, int &qi) {
+        if constexpr (W >= LOB_CXL2_W) {
+            // ONE pass, ONE group minimum: each thread's lowest exact-OID row and lowest
+            // synthetic row at P (with their Q), keyed so that any exact match in the group
+            // beats every synthetic one: exact -> slot, synthetic -> NP + slot, none -> 2 NP.
+            // The owner's captured Q is the found order's (its lowest match is the slot).
+            unsigned rex = KPL, rsy = KPL;
+            int qex = 0, qsy = 0;
+#pragma unroll
+            for (int j = R - 1; j >= 0; --j) {
+                const int q = bk.hot(SD, F_Q, j), o = bk.hot(SD, F_OID, j);
+                if (q > 0 && o == mOID) { rex = (unsigned)j; qex = q; }
+                if (q > 0 && o <= -9000 && bk.hot(SD, F_P, j) == mP) { rsy = (unsigned)j; qsy = q; }
+            }
+            const unsigned key = rex < (unsigned)KPL
+                                     ? rex * GT + (unsigned)tid
+                                     : (rsy < (unsigned)KPL ? (unsigned)BK::NP + rsy * GT + (unsigned)tid : 2u * BK::NP);
+            const unsigned k = gmin_u(key);
+            const bool exact = k < (unsigned)BK::NP;
+            qi = exact ? qex : qsy;
+            return (int)(exact ? k : k - BK::NP);  // >= NP when neither exists
+        } else {
+            // exact OID first, then the synthetic fallback (G12); the scans capture
+            // the Q of each thread's lowest matching row (the owner's is the found order's):
+            // no select chain after the reduction (C5 N = 512 +8 %, C4 / C2 +0.3 %)
+            int slot = lowest_rows_q<SD, R>(qi, [&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
+            if (!found(slot))
+                slot = lowest_rows_q<SD, R>(qi, [&](int j) {
+                    return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
+                });
+            return slot;
+        }
+    }
     template <int SD, int R>
     __device__ __forceinline__ void cancel_r(int mQ, int mP, int mOID) {
-#if LOB_CXL == 2
-        // ONE pass, ONE group minimum: each thread's lowest exact-OID row and lowest
-        // synthetic row at P (with their Q), keyed so that any exact match in the group
-        // beats every synthetic one: exact -> slot, synthetic -> NP + slot, none -> 2 NP.
-        // The owner's captured Q is the found order's (its lowest match is the slot).
-        unsigned rex = KPL, rsy = KPL;
-        int qex = 0, qsy = 0;
-#pragma unroll
-        for (int j = R - 1; j >= 0; --j) {
-            const int q = bk.hot(SD, F_Q, j), o = bk.hot(SD, F_OID, j);
-            if (q > 0 && o == mOID) { rex = (unsigned)j; qex = q; }
-            if (q > 0 && o <= -9000 && bk.hot(SD, F_P, j) == mP) { rsy = (unsigned)j; qsy = q; }
-        }
-        const unsigned key = rex < (unsigned)KPL ? rex * GT + (unsigned)tid
-                                                 : (rsy < (unsigned)KPL ? (unsigned)BK::NP + rsy * GT + (unsigned)tid
-                                                                        : 2u * BK::NP);
-        const unsigned k = gmin_u(key);
-        if (k >= 2u * BK::NP) {                    // G15
-            if constexpr (PRED) add64_if0(tid, sc + 8u * ST_UNKNOWN, 1);
-            else if (tid == 0) count(ST_UNKNOWN, 1);
-            return;
-        }
-        const bool exact = k < (unsigned)BK::NP;
-        const int slot = (int)(exact ? k : k - BK::NP);
-        const bool own = tid == (slot & (GT - 1));
-        const int j = slot / GT;
-        const int qi = exact ? qex : qsy;          // meaningful on the owner
-#elif LOB_CXL == 1
-        // the scans capture the Q of each thread's lowest matching row (the owner's is the
-        // found order's): no select chain after the reduction
         int qi = 0;
-        int slot = lowest_rows_q<SD, R>(qi, [&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
-        if (!found(slot))
-            slot = lowest_rows_q<SD, R>(qi, [&](int j) {
-                return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
-            });
-        if (!found(slot)) {                        // G15
-            if constexpr (PRED) add64_if0(tid, sc + 8u * ST_UNKNOWN, 1);
-            else if (tid == 0) count(ST_UNKNOWN, 1);
-            return;
-        }
-        const bool own = tid == (slot & (GT - 1));
-        const int j = slot / GT;
-#else
-        int slot = lowest_rows<R>([&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
-        if (!found(slot))
-            slot = lowest_rows<R>([&](int j) {
-                return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
-            });
+        const int slot = cancel_find<SD, R>(mP, mOID, qi);
         if (!found(slot)) {                        // G15
             if constexpr (PRED) add64_if0(tid, sc + 8u * ST_UNKNOWN, 1);
             else if (tid == 0) count(ST_UNKNOWN, 1);
@@ -760,8 +748,6 @@ struct Engine {
         }
         const bool own = tid == (slot & (GT - 1));
         const int j = slot / GT;                   // the slot is occupied: its row is below R
-        const int qi = bk.template get_r<R>(SD, F_Q, j);
-#endif
         const int cq = (mQ < qi) ? mQ : qi;
         if (own) part_cxl += cq;                   // G14
         bk.template put_if_r<R>(own, SD, F_Q, j, qi - mQ);  // Q <= 0 -> empty
@@ -953,6 +939,10 @@ struct Engine {
         outp = -1; outq = 0;
         const int h = hr[SD];
         if (h < 0) return;
+#if LOB_L2FULL
+        if constexpr (KPL >= 8) l2_rows<SD, KPL>(L, outp, outq);
+        else
+#endif
         with_rows(h, [&](auto R) { l2_rows<SD, R>(L, outp, outq); });
         bool bg = false;
 #pragma unroll
@@ -1156,8 +1146,13 @@ constexpr int step_smem_bytes() {
 // MODE 3 = MODE 0 built for 8 CTAs/SM (64 registers); chosen by the host for many-wave
 // batches of 4-row books.  (With the uniform persistent loop MODE 0 also fits in 64
 // registers without spills, so the two now compile alike; MODE 3 keeps the hard cap.)
+// resident CTAs per SM the register budget is sized for
+template <int KPL, int W, int MODE>
+constexpr int step_min_blocks() {
+    return MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? (KPL > 8 ? MINB16 : 3) : (KPL > 8 ? 12 / W : 16 / W))));
+}
 template <int KPL, int W, int G, int MODE>
-__global__ void __launch_bounds__(32 * W * G, (MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? (KPL > 8 ? MINB16 : 3) : (KPL > 8 ? 12 / W : 16 / W))))))
+__global__ void __launch_bounds__(32 * W * G, step_min_blocks<KPL, W, MODE>())
     lob_step(const Params p, const EnvParams ep) {
     using BK = RegBook<KPL, W>;
     constexpr bool TL1 = MODE == 1, ENV = MODE == 2;

@@ -1,18 +1,20 @@
 #!/bin/bash
-# All round-end evidence for the in-tree build in one gpurun call.
+# All round evidence for the in-tree build in one gpurun call.
 #   scripts/final_evidence.sh <tag>
 cd "$(dirname "$0")/.."
 tag=${1:-final}
+mkdir -p gpurun_out
 bash scripts/measure_v.sh $tag
+bash scripts/ncu_configs.sh $tag C2 C3 C5_512 C5_2048 > gpurun_out/ncu_configs_$tag.txt 2>&1
 CONFIGS="C1 C2 C3 C4 C5_32 C5_100 C5_256 C5_512 C5_1024 C5_2048" bash scripts/config_sweep.sh > /dev/null
 timeout 300 python scripts/rl_shape.py > gpurun_out/rl_shape_$tag.json 2>&1
-timeout 300 python scripts/env_bench.py > gpurun_out/env_bench_$tag.json 2>&1
-LOB_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
-  --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 3 > gpurun_out/bench_gloo2_$tag.json 2> gpurun_out/bench_gloo2_$tag.err
+timeout 600 python scripts/env_bench.py > gpurun_out/env_bench_$tag.json 2>&1
+timeout 300 python scripts/session_overhead.py > gpurun_out/session_overhead_$tag.json 2>&1
+LOB_DIST_BACKEND=gloo timeout 600 python bench.py --gpus 2 --steps 5 --warmup 3 > gpurun_out/bench_gloo2_$tag.json 2> gpurun_out/bench_gloo2_$tag.err
 timeout 300 python bench.py --l1 --steps 5 --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_l1_$tag.json 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$tag.json 2>&1
-bash scripts/sanitize_all.sh > gpurun_out/sanitize_$tag.txt
-bash scripts/k_sweep.sh > /dev/null
 timeout 300 python scripts/paper_tables.py > gpurun_out/paper_tables_$tag.json 2>&1
 timeout 300 taskset -c 0 python scripts/oracle_1core.py > gpurun_out/oracle_1core_$tag.json 2>&1
-cat gpurun_out/measure_$tag.txt gpurun_out/sweep.txt gpurun_out/sanitize_$tag.txt gpurun_out/k_sweep.txt
+bash scripts/k_sweep.sh > /dev/null
+bash scripts/sanitize_all.sh > gpurun_out/sanitize_$tag.txt
+cat gpurun_out/measure_$tag.txt gpurun_out/ncu_configs_$tag.txt gpurun_out/sweep.txt gpurun_out/sanitize_$tag.txt gpurun_out/k_sweep.txt

@@ -59,4 +59,15 @@ for N, K in [(100, 9), (2048, 2)]:
         env.step(acts, torch.from_numpy(np.ascontiguousarray(msgs[:, s * 20:(s + 1) * 20])))
     torch.cuda.synchronize()
     print("env", N, "ok")
+    # the same steps through a resident session (N3 residency), from the same books
+    be.init(torch.from_numpy(init), lobgen.INIT_TS, lobgen.INIT_TNS)
+    env.reset(lobgen.INIT_TS, lobgen.INIT_TNS)
+    from paper_2308_13289_b200 import LobSession  # noqa: E402
+    sess = LobSession(env, torch.from_numpy(np.ascontiguousarray(msgs[:, :60])), 3)
+    rng = np.random.default_rng(N)
+    for s in range(3):
+        sess.step(torch.from_numpy(rng.uniform(0, 300, (K, 4)).astype(np.float32)))
+    sess.end()
+    torch.cuda.current_stream().synchronize()
+    print("session", N, "ok")
 sys.exit(1 if fails else 0)
