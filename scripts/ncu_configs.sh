@@ -9,4 +9,7 @@ for c in "$@"; do
     --clock-control none --import-source on -k regex:lob_step -s 3 -c 1 -o gpurun_out/prof_${c}_$tag -f \
     python bench.py --config $c --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline --parity-books 0 > gpurun_out/ncu_${c}_$tag.log 2>&1
   echo "$c ncu rc=$?"
+  case $c in C2) n=10000000;; C3) n=16384000;; C4) n=65536000;; C1) n=1000;; *) n=4096000;; esac
+  python scripts/ncu_summary.py full gpurun_out/prof_${c}_$tag.ncu-rep $n > gpurun_out/step_${c}_ncu_full_$tag.txt 2>&1
+  [ -n "$KEEP_REPS" ] || { mkdir -p /tmp/ncu_reps && mv gpurun_out/prof_${c}_$tag.ncu-rep /tmp/ncu_reps/; }
 done

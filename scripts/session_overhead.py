@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Per-step cost of the resident session vs the per-step fused launch (CUDA graph), at
 two data sizes per step (M = 100 and M = 1), 1,000 envs of N = 100: separates the fixed
-per-step cost (release / wait, launch, book load / store) from the per-message cost.
-Prints one JSON line."""
+per-step cost (release / wait, launch, book load / store) from the per-message cost;
+then both at M = 100 for larger books (N = 512: 1,000 envs; N = 2048: 400 envs), where
+the per-step book load / store the session avoids is larger.  Prints one JSON line."""
 import json
 import os
 import sys
@@ -16,10 +17,10 @@ import lobgen  # noqa: E402
 from paper_2308_13289_b200 import EnvConfig, LobBatch, LobEnv, LobSession  # noqa: E402
 
 
-def run(K, M, steps):
-    cfg = lobgen.Config("env", K, 100, steps, M, 10, 256, 10, "lobster", 7)
+def run(K, M, steps, N=100):
+    cfg = lobgen.Config("env", K, N, steps, M, min(N // 3, 33), 256, 10, "lobster", 7)
     msgs, init = lobgen.generate(cfg)
-    b = LobBatch(K, 100, 256, 10)
+    b = LobBatch(K, N, 256, 10)
     ti = torch.from_numpy(init).cuda()
     env = LobEnv(b, EnvConfig(-1, 10**6, 2, 100, 3600, 77, 2_000_000_000, 0, 0.0), M)
     dall = torch.from_numpy(msgs).cuda()
@@ -98,5 +99,6 @@ if __name__ == "__main__":
     for M in (100, 1):
         res[M] = run(1000, M, 100 if M == 1 else 20)
     t = {k: (res[100][k] - res[1][k]) / 99 for k in res[100]}
-    print(json.dumps({"M100": res[100], "M1": res[1], "per_message_us": t,
-                      "fixed_us_per_step": {k: res[1][k] - t[k] for k in t}}))
+    big = {f"N{N}_K{K}_M100": run(K, 100, 20, N) for N, K in ((512, 1000), (2048, 400))}
+    print(json.dumps({"N100_K1000_M100": res[100], "N100_K1000_M1": res[1], "per_message_us": t,
+                      "fixed_us_per_step": {k: res[1][k] - t[k] for k in t}, **big}))
