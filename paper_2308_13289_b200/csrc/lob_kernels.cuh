@@ -39,6 +39,9 @@
 #ifndef LOB_R16   // row bounds of 16-row books: 1 = {8,16} (C5 N = 512 +24 %, N = 2048 +5 % over
 #define LOB_R16 1 // 0 = {4,8,16}); 2 = {16} (-25 %), 3 = {4,16} (-46 %, -23 %)
 #endif
+#ifndef LOB_ROWR   // the add's register write through a compare chain (not the row switch)
+#define LOB_ROWR 4  // for books of <= LOB_ROWR rows at the full row bound (C2 +0.5 %, C3 +0.4 %, C4 -0.1 %)
+#endif
 #ifndef LOB_TREE  // get_r as a select tree for row bounds >= LOB_TREE (0 = never; 16: C5 N = 512
 #define LOB_TREE 0  // +6 % before the {8,16} row bounds, +-0 after)
 #endif
@@ -844,6 +847,7 @@ struct Engine {
         };
         // the slot's row is at most R: a compare chain instead of the jump table
         if constexpr (R < KPL) bk.template row_r<R + 1>(slot / GT, put);
+        else if constexpr (KPL <= LOB_ROWR) bk.template row_r<KPL>(slot / GT, put);
         else bk.row(slot / GT, put);
         if constexpr (PRED) sts128_if0(tid, bk.rec(OWN, slot), make_int4(mOID, mTID, mTS, mTNS));  // one writer
         else if (tid == 0) bk.put_cold(OWN, slot, make_int4(mOID, mTID, mTS, mTNS));

@@ -20,6 +20,9 @@
 namespace lobk {
 
 constexpr unsigned SESSION_STOP = 0x80000000u;
+#ifndef SESS_POLL_NS
+#define SESS_POLL_NS 32  // back-off between polls of the step flag / the done counter
+#endif
 
 struct SessionParams {
     const unsigned *go;  // step flag (caller's stream)
@@ -33,6 +36,11 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
     return v;
 }
 
+// a release reduction: the CTA's writes (ordered before it by the barrier) are visible
+// to whoever acquires the counter -- no separate full fence
+__device__ __forceinline__ void red_release_gpu_add(unsigned *p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -48,7 +56,7 @@ __global__ void lob_session_sync_kernel(unsigned *go, unsigned s, const unsigned
     if (threadIdx.x != 0) return;
     st_release_gpu(go, s);
     if (target == 0u) return;
-    while ((int)(ld_acquire_gpu(done) - target) < 0) __nanosleep(20);
+    while ((int)(ld_acquire_gpu(done) - target) < 0) __nanosleep(SESS_POLL_NS);
 }
 
 // Step boundary of a whole CTA (every group, with or without a book, calls it):
@@ -67,15 +75,12 @@ __global__ void lob_session_sync_kernel(unsigned *go, unsigned s, const unsigned
 __device__ __forceinline__ unsigned session_step_sync(const SessionParams &sp, unsigned s, bool signal,
                                                       unsigned *word) {
     __syncthreads();
-    if (signal && threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(sp.done, 1u);
-    }
+    if (signal && threadIdx.x == 0) red_release_gpu_add(sp.done, 1u);
     const unsigned wid = __reduce_min_sync(FULL, threadIdx.x / 32u);  // uniform
     if (wid == 0u) {
         unsigned v = ld_acquire_gpu(sp.go);
         while (__reduce_min_sync(FULL, ((v & SESSION_STOP) != 0u || v >= s) ? 1u : 0u) == 0u) {
-            __nanosleep(64);
+            __nanosleep(SESS_POLL_NS);
             v = ld_acquire_gpu(sp.go);
         }
         v = __reduce_max_sync(FULL, v);
@@ -212,10 +217,7 @@ __global__ void __launch_bounds__(32 * W * G, (KPL <= 4 ? 5 : (W == 1 ? (KPL > 8
     }
     if (steps_done == sp.n_steps) {  // the last step's signal (the loop ended without a boundary)
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(sp.done, 1u);
-        }
+        if (threadIdx.x == 0) red_release_gpu_add(sp.done, 1u);
     }
     if (!has) return;
     // chunks still in flight land before the CTA exits (stopped sessions)
