@@ -216,17 +216,22 @@ int lob_env_step(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const flo
  *  d_work, d_reward, d_done, d_executed, d_l2_out ([K][L][4], nullable): the same
  *    outputs as lob_env_step, overwritten by every step, complete on cuda_stream after
  *    lob_session_step returns (stream order).
- * lob_session_step enqueues on cuda_stream a release of the next step (a stream memory
- * write) and a wait until every book has finished it (a stream memory wait); the host
- * does not block.  Between begin and end the trade log and its count are per step (as
- * after a lob_env_step); the book (lob_get_book) and the counters are updated at end.
+ * lob_session_step enqueues ONE 32-thread kernel on cuda_stream that releases the next
+ * step (a release store to a device flag) and spins until every CTA of the session has
+ * finished it; the host does not block, and the call can be captured into a CUDA graph
+ * (with capture started on a side stream: see the synchronisation rule below).
+ * Between begin and end the trade log and its count are per step (as after a
+ * lob_env_step); the book (lob_get_book) and the counters are updated at end.
  * Requirements: one session per context; msgs_per_step >= 1; every book resident at
- * once (ceil(K / books per CTA) CTAs in one wave of the GPU, else LOB_EUNSUPPORTED; the
- * launch is cooperative); at most n_steps steps (then LOB_EINVAL); the driver's stream
- * memory operations (else LOB_EUNSUPPORTED).  Calls on the context other than
- * lob_session_* while a session runs are undefined, and a DEVICE-wide synchronisation
- * (cudaDeviceSynchronize) deadlocks: it waits for the resident kernel, which waits for
- * the next step -- synchronise streams instead.  lob_destroy stops a running session. */
+ * once (ceil(K / books per CTA) CTAs in one wave of the GPU, else LOB_EUNSUPPORTED);
+ * at most n_steps steps (then LOB_EINVAL).  (Test hook LOB_SESSION_MEMOPS=1: release and
+ * wait by the driver's stream memory operations instead; LOB_EUNSUPPORTED if absent.)
+ * Rules while a session runs: calls on the context other than lob_session_* are
+ * undefined; a DEVICE-wide synchronisation (cudaDeviceSynchronize, torch.cuda.graph's
+ * entry) deadlocks -- it waits for the resident kernel, which waits for the next step --
+ * so synchronise streams instead; under lazy module loading, launch every kernel the
+ * step loop uses once before lob_session_begin (a first launch loads its module, and
+ * the load waits for the device).  lob_destroy stops a running session. */
 int lob_session_begin(lob_ctx *ctx, void *d_env, const lob_env_config *cfg, const float *d_actions,
                       const int32_t *d_data, int32_t n_steps, int32_t msgs_per_step, int32_t *d_work,
                       double *d_reward, int32_t *d_done, int64_t *d_executed, int32_t *d_l2_out,
