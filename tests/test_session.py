@@ -159,3 +159,20 @@ def test_session_errors_and_destroy_while_running():
     del s2, env
     b.__del__()
     torch.cuda.synchronize()  # the kernel has exited
+
+
+def test_session_memops_hook(monkeypatch):
+    """The A/B hook LOB_SESSION_MEMOPS=1 (release / wait by the driver's stream memory
+    operations instead of the step launch) gives the same results."""
+    from paper_2308_13289_b200 import LobSession
+    monkeypatch.setenv("LOB_SESSION_MEMOPS", "1")
+    K = 100
+    cfg, msgs, b, env, oe, oenv = _setup(K, 100, -1, 1800, 11, steps=4)
+    sess = LobSession(env, torch.from_numpy(msgs), cfg.n_steps)
+    rng = np.random.default_rng(3)
+    prev = np.zeros(K, np.int64)
+    for s in range(cfg.n_steps):
+        acts = rng.uniform(0, 400, (K, 4)).astype(np.float32)
+        prev = _check_step(s, env, sess, oe, oenv, acts, np.ascontiguousarray(msgs[:, s * 100:(s + 1) * 100]), prev)
+    sess.end()
+    np.testing.assert_array_equal(b.book().cpu().numpy(), oe.book())
