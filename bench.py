@@ -150,14 +150,22 @@ class ClockSampler:
 
     def __enter__(self):
         if self.ok:
+            self._sample()                     # warm NVML outside the region ...
+            self.samples.clear()
+            self.reasons.clear()
+            # ... and let the sampler thread in often while the host enqueues
+            self._sw = sys.getswitchinterval()
+            sys.setswitchinterval(0.0005)
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
 
     def __exit__(self, *a):
         if self.ok:
+            self._sample()                     # at least one sample at the end of the region
             self._stop.set()
             self.t.join()
+            sys.setswitchinterval(self._sw)
 
     def summary(self):
         if not self.ok or not self.samples:
@@ -377,6 +385,8 @@ class Phase:
             for i in range(args.steps):
                 self.step(stream, kev[i])
             end.record(stream)
+            while not end.query():             # poll (GIL released in sleep) so the clock
+                time.sleep(0.0005)             # sampler runs during the device work
             torch.cuda.synchronize()
         self.n_launch = launch_count() - n_launch0
         if self.world > 1:
