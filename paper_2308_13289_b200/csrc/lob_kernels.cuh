@@ -42,6 +42,9 @@
 #ifndef LOB_ROWR   // the add's register write through a compare chain (not the row switch)
 #define LOB_ROWR 4  // for books of <= LOB_ROWR rows at the full row bound (C2 +0.5 %, C3 +0.4 %, C4 -0.1 %)
 #endif
+#ifndef LOB_SYNC_READER  // one-warp books: the __syncwarp that publishes a new order's cold
+#define LOB_SYNC_READER 1   // record runs where other lanes read records (the arg-best), not per
+#endif                      // add (C2 +1.6 %, C3 / C5 N = 100 +0.8 %, N = 256 +1.9 %; racecheck clean)
 #ifndef LOB_TREE  // get_r as a select tree for row bounds >= LOB_TREE (0 = never; 16: C5 N = 512
 #define LOB_TREE 0  // +6 % before the {8,16} row bounds, +-0 after)
 #endif
@@ -387,6 +390,10 @@ struct Engine {
     // best order's (Ts, Tns): uniform registers for multi-warp books (no barriers),
     // shared memory for warp books (4 registers fewer in the 64-register kernel)
     static constexpr bool kBtRegs = (W > 1);
+    // where a new order's cold record is published to the other lanes (LOB_SYNC_READER):
+    // at the reader (the arg-best), except in the many-wave build (PRED), where the
+    // per-add __syncwarp measured as fast (C4 -0.2 % the other way)
+    static constexpr bool kSyncReader = LOB_SYNC_READER && W == 1 && !PRED;
     int bTS[2], bTNS[2];
     int hr[2];              // row high-water mark per side (see with_rows)
     unsigned long long bV[2];  // TL1: total quantity at the cached best price (its L1 volume,
@@ -571,6 +578,7 @@ struct Engine {
         }
         const unsigned m = gmin_u(lk);
         if (m == 0xffffffffu) { set_empty<SD>(); return; }
+        if constexpr (kSyncReader) __syncwarp();  // cold records written by lane 0 (add_r)
         // candidates at the best price: thread-local earliest (Ts, Tns, row)
         int lts = INT_MAX, ltns = INT_MAX, lj = -1, lc = 0;
         unsigned long long lv = 0;
@@ -855,7 +863,7 @@ struct Engine {
         // records are read only inside recompute_best_multi, after its first barrier,
         // and every such read completes before its second barrier, so the barriers
         // already order this write against earlier and later reads.
-        if constexpr (W == 1) group_sync<W>();
+        if constexpr (W == 1 && !kSyncReader) group_sync<W>();
         if constexpr (TL1) {  // level volume: a new best level, or one more order at the best price
             const int ob = bslot[OWN], op = bP[OWN];
             const bool lvl = ob == BEST_EMPTY || (ob >= 0 && ((OWN == ASK) ? mP < op : mP > op));

@@ -176,3 +176,48 @@ def test_session_memops_hook(monkeypatch):
         prev = _check_step(s, env, sess, oe, oenv, acts, np.ascontiguousarray(msgs[:, s * 100:(s + 1) * 100]), prev)
     sess.end()
     np.testing.assert_array_equal(b.book().cpu().numpy(), oe.book())
+
+
+def test_session_steps_in_cuda_graph():
+    """A whole episode's steps captured once in a CUDA graph after lob_session_begin (on a
+    side stream with capture_begin / capture_end: torch.cuda.graph() would synchronise the
+    device, i.e. wait for the resident kernel) and replayed: per-step rewards, executed
+    quantities and L2, and the final books equal the oracle env."""
+    from paper_2308_13289_b200 import LobSession
+    K, S = 200, 6
+    cfg, msgs, b, env, oe, oenv = _setup(K, 100, 1, 1800, 21, steps=S)
+    rng = np.random.default_rng(8)
+    acts_h = [rng.uniform(0, 300, (K, 4)).astype(np.float32) for _ in range(S)]
+    acts = [torch.from_numpy(a).cuda() for a in acts_h]
+    rew = torch.zeros((S, K), dtype=torch.float64, device="cuda")
+    ex = torch.zeros((S, K), dtype=torch.int64, device="cuda")
+    l2s = torch.zeros((S, K, 10, 4), dtype=torch.int32, device="cuda")
+    cur = torch.cuda.current_stream()
+    sess = LobSession(env, torch.from_numpy(msgs), S)
+    # every kernel the captured loop uses has run once (lazy module loading, see lob.h)
+    sess.actions.copy_(acts[0]); rew[0].copy_(env.reward); ex[0].copy_(env.executed); l2s[0].copy_(sess.l2)
+    cs = torch.cuda.Stream()
+    cs.wait_stream(cur)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(cs):
+        g.capture_begin(capture_error_mode="relaxed")
+        for s in range(S):
+            sess.actions.copy_(acts[s])
+            sess.step(None)
+            rew[s].copy_(env.reward)
+            ex[s].copy_(env.executed)
+            l2s[s].copy_(sess.l2)
+        g.capture_end()
+    cur.wait_stream(cs)
+    g.replay()
+    sess.end()
+    cur.synchronize()
+    prev = np.zeros(K, np.int64)
+    for s in range(S):
+        ro, do, xo, am = oenv.step(acts_h[s], np.ascontiguousarray(msgs[:, s * 100:(s + 1) * 100]), 100)
+        np.testing.assert_array_equal(ex[s].cpu().numpy(), xo, err_msg=f"executed step {s}")
+        np.testing.assert_array_equal(l2s[s].cpu().numpy(), oe.l2(), err_msg=f"L2 step {s}")
+        scale = (xo - prev).astype(np.float64) * 4e6 * 1.5
+        assert np.all(np.abs(rew[s].cpu().numpy() - ro) <= 1e-12 * np.maximum(1.0, scale)), s
+        prev = xo.copy()
+    np.testing.assert_array_equal(b.book().cpu().numpy(), oe.book())
