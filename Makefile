@@ -9,7 +9,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xptxas -
 PKG       := paper_2308_13289_b200
 LIB       := $(PKG)/liblob.so
 SRCS      := $(PKG)/csrc/lob_api.cu
-DEPS      := $(SRCS) $(PKG)/csrc/lob_kernels.cuh $(PKG)/csrc/lob_env.cuh $(PKG)/csrc/lob_session.cuh include/lob.h
+DEPS      := $(SRCS) $(PKG)/csrc/lob_kernels.cuh $(PKG)/csrc/lob_env.cuh $(PKG)/csrc/lob_session.cuh $(PKG)/csrc/lob_split.cuh include/lob.h
 # provenance: hash of the engine sources + this Makefile (flags), exported by lob_build_id()
 BUILD_ID  := $(shell cat $(DEPS) Makefile | sha256sum | cut -c1-16)
 

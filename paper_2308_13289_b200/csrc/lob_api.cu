@@ -15,6 +15,7 @@
 #include "lob_kernels.cuh"
 #include "lob_env.cuh"
 #include "lob_session.cuh"
+#include "lob_split.cuh"
 
 using namespace lobk;
 
@@ -89,6 +90,9 @@ struct lob_ctx {
     int sm_count;
     Geo geo;
     int grid_cap[4];  // persistent grid: resident CTAs of the step kernel, per MODE
+    long long split_max;  // side-split build (lob_split.cuh) for launches of at most this many
+                          // books (LOB_SPLIT_BPS books per SM; 0 = never) ...
+    long long split_min_msgs;  // ... of at least this many messages per book (LOB_SPLIT_MIN_MSGS)
     bool force_wide;  // test hook (env LOB_FORCE_WIDE=1): MODE 3 for every 4-row batch
     int grid_limit;   // test hook (env LOB_GRID_CAP=n): at most n CTAs per step launch, so
                       // small batches exercise the dynamic book scheduler
@@ -115,6 +119,18 @@ struct lob_ctx {
 #ifndef G16
 #define G16 4
 #endif
+// The side-split build (lob_split.cuh) for latency-bound launches: at most LOB_SPLIT_BPS
+// books per SM and at least LOB_SPLIT_MIN_MSGS messages per book.  Measured on B200
+// (profiles/r02_v32_split_sweep.txt): C2 (1,000 books x 10,000 messages) +5 %; C1 -6 %,
+// C4 batches of 592 - 4,736 books (1,000 messages) -5 ... -38 %, so only long streams of
+// few books take it.
+#ifndef LOB_SPLIT_BPS
+#define LOB_SPLIT_BPS 8
+#endif
+#ifndef LOB_SPLIT_MIN_MSGS
+#define LOB_SPLIT_MIN_MSGS 4096
+#endif
+constexpr int GS = 2;  // books (warp pairs) per CTA of the side-split build
 namespace {
 // call f(IC<KPL>, IC<W>, IC<G>) for the compiled geometry (G = books per CTA)
 template <class F>
@@ -171,6 +187,14 @@ int launch_step(lob_ctx *ctx, const int32_t *d_msgs, int32_t n_steps, int32_t M,
         unsigned grid = need < cap ? need : cap;
         if (ctx->grid_limit > 0 && grid > (unsigned)ctx->grid_limit) grid = (unsigned)ctx->grid_limit;
         const int smem = step_smem_bytes<KPL, W, G>();
+        if constexpr (W == 1) {
+            if (!env && !d_l1 && nb <= ctx->split_max && (long long)n_steps * M >= ctx->split_min_msgs &&
+                !ctx->force_wide && ctx->grid_limit == 0) {  // few books: one warp per side (lob_split.cuh)
+                lob_step_split<KPL, GS><<<blocks_for(nb, GS), 64 * GS, GS * SplitLayout<KPL>::BYTES, st>>>(p);
+                rc = after_launch("lob_step_split kernel");
+                return;
+            }
+        }
         if (env) lob_step<KPL, W, G, 2><<<grid, 32 * W * G, smem, st>>>(p, ep);
         else if (d_l1) lob_step<KPL, W, G, 1><<<grid, 32 * W * G, smem, st>>>(p, ep);
         else if constexpr (kWide) {
@@ -219,6 +243,10 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
         c->force_wide = fw && fw[0] == '1';
         const char *gc = getenv("LOB_GRID_CAP");
         c->grid_limit = gc ? atoi(gc) : 0;
+        const char *sb = getenv("LOB_SPLIT_BPS");
+        c->split_max = (long long)sms * (sb ? atoi(sb) : LOB_SPLIT_BPS);
+        const char *sm = getenv("LOB_SPLIT_MIN_MSGS");
+        c->split_min_msgs = sm ? atoll(sm) : LOB_SPLIT_MIN_MSGS;
     }
     int per_sm[4] = {1, 1, 1, 1}, sess_per_sm = 0;
     int rc = LOB_OK;
@@ -242,6 +270,11 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state) {
             if (e == cudaSuccess)
                 e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[3], lob_step<KPL, W, G, 3>, 32 * W * G,
                                                                   smem);
+        }
+        if constexpr (W == 1) {
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(lob_step_split<KPL, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GS * SplitLayout<KPL>::BYTES);
         }
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(lob_session<KPL, W, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -724,6 +757,20 @@ int lob_trace_read(int64_t *h_msg, int64_t *h_l2) {
     cudaError_t e = cudaMemcpyFromSymbol(h_msg, g_trace_msg, sizeof(g_trace_msg));
     if (e == cudaSuccess) e = cudaMemcpyFromSymbol(h_l2, g_trace_l2, sizeof(g_trace_l2));
     return e == cudaSuccess ? LOB_OK : cuda_fail(e, "trace read");
+}
+#endif
+
+#ifdef LOB_SPLIT_STATS
+// instrumented variant only: the side-split build's wait counters, then reset
+int lob_split_stats_read(uint64_t *h) {
+    cudaError_t e = cudaMemcpyFromSymbol(h, g_split_stats, sizeof(g_split_stats));
+    static const unsigned long long z[4][3] = {};
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_split_stats, z, sizeof(z));
+    return e == cudaSuccess ? LOB_OK : cuda_fail(e, "split stats read");
+}
+int lob_split_trace_read(int64_t *h) {
+    cudaError_t e = cudaMemcpyFromSymbol(h, g_split_trace, sizeof(g_split_trace));
+    return e == cudaSuccess ? LOB_OK : cuda_fail(e, "split trace read");
 }
 #endif
 

@@ -400,6 +400,8 @@ struct Engine {
                                // exact in 64 bits; reported saturated at INT32_MAX, G20)
     long long part_cxl;     // cancelled quantity, accumulated on the owner thread (G14)
     long long part_trd;     // traded quantity, accumulated on the owner thread
+    int lastPs;             // price of the last fill (side-split build: a bound on the side's
+                            // best after its best order was filled away; lob_split.cuh)
 
     __device__ __forceinline__ Engine(const Params &p_) : p(p_) {}
 
@@ -798,6 +800,7 @@ struct Engine {
             if (s < 0) break;                                      // side empty
             const int Ps = bP[OPP];
             if (OWN == BID ? (Pa < Ps) : (Pa > Ps)) break;         // prices do not overlap
+            lastPs = Ps;
             const int ol = s & (GT - 1);
             const bool own = tid == ol;
             const int sj = s / GT;

@@ -90,7 +90,7 @@ def test_product_path_never_touches_the_oracle():
 
 def test_step_kernels_are_warp_uniform():
     """Performance guard ("uniform persistent loop"): the one-warp
-    step kernels (plain, L1-trace, many-wave, fused env step, resident session) must compile with the persistent loop proven warp-uniform -- no
+    step kernels (plain, L1-trace, many-wave, fused env step, resident session, side-split) must compile with the persistent loop proven warp-uniform -- no
     divergence checks (BRA.DIV) before warp collectives.  ptxas's convergence proof is
     fragile (an unrelated source edit once cost C4 15 % through ~17 extra control
     instructions per message), so the SASS is checked here, without a GPU."""
@@ -100,14 +100,16 @@ def test_step_kernels_are_warp_uniform():
     checked = 0
     for f in funcs:
         m = re.match(r"_ZN4lobk8lob_stepILi(\d+)ELi1ELi4ELi([0-3])E", f) or \
-            re.match(r"_ZN4lobk11lob_sessionILi(\d+)ELi1ELi4E()", f)
+            re.match(r"_ZN4lobk11lob_sessionILi(\d+)ELi1ELi4E()", f) or \
+            re.match(r"_ZN4lobk14lob_step_splitILi(\d+)ELi2E()", f)
         if not m:
             continue
         checked += 1
         n_div = f.count("BRA.DIV")
         assert n_div == 0, f"{f[:40]} (KPL={m.group(1)}, W=1, MODE={m.group(2)}) has {n_div} BRA.DIV"
-    # MODE 0 (step), 1 (L1 trace), 2 (fused env step), 3 (many-wave step), resident session
-    assert checked >= 25, checked
+    # MODE 0 (step), 1 (L1 trace), 2 (fused env step), 3 (many-wave step), resident session,
+    # side-split step (lob_split.cuh)
+    assert checked >= 31, checked
 
 
 def test_bench_kernel_register_budget():

@@ -101,6 +101,26 @@ def test_dynamic_scheduling_small_grid(monkeypatch, N, cap, wide, calls):
     assert_outputs_equal(g, o, what=f"dyn N={N} cap={cap} wide={wide} calls={calls}")
 
 
+@pytest.mark.parametrize("split", [0, 1])
+@pytest.mark.parametrize("profile,N,Tcap,calls", [("heavy_market", 100, 1024, 1), ("heavy_market", 32, 5, 3),
+                                                  ("lobster", 100, 100, 1), ("ties", 64, 1024, 2),
+                                                  ("garbage", 256, 200, 1), ("synthetic", 512, 1024, 1),
+                                                  ("overflow", 16, 1024, 4), ("cancel_heavy", 97, 0, 1),
+                                                  ("saturate", 130, 1024, 1), ("heavy_market", 1, 1024, 1)])
+def test_side_split_build(monkeypatch, split, profile, N, Tcap, calls):
+    # the side-split build (lob_split.cuh: one warp per side, ring hand-off of Q_a',
+    # trade-order waits) forced on (LOB_SPLIT_BPS large: also several waves of warp pairs)
+    # and off (0: lob_step on a small batch); deep sweeps with every trade logged
+    # (Tcap >= fills: the trade-order wait on every fill), tiny and empty logs, ties,
+    # malformed messages, synthetic cancels, saturated sides, one-slot books
+    monkeypatch.setenv("LOB_SPLIT_BPS", "100000" if split else "0")
+    monkeypatch.setenv("LOB_SPLIT_MIN_MSGS", "0")
+    K = 1900 if split and N <= 128 else 300
+    cfg = lobgen.Config("s", K, N, 6, 64, min(N, 30), Tcap, 10, profile, 11 * N + Tcap + calls)
+    g, o = _both(cfg, calls=calls)
+    assert_outputs_equal(g, o, what=f"split={split} {profile} N={N} Tcap={Tcap} calls={calls}")
+
+
 @pytest.mark.parametrize("L,Tcap", [(1, 0), (32, 3), (10, 1)])
 def test_levels_and_tiny_trade_log(L, Tcap):
     cfg = lobgen.Config("p", 200, 100, 5, 50, 40, Tcap, L, "heavy_market", 5)
