@@ -88,7 +88,10 @@ int lob_create(lob_ctx **out, const lob_config *cfg, void *d_state);
 /* Test hooks, read from the environment by lob_create (results never change, only
  * the launch shape): LOB_FORCE_WIDE=1 launches the many-wave build of the step
  * kernel for every 4-row batch; LOB_GRID_CAP=n caps the persistent grid at n CTAs,
- * so small batches run through the dynamic book scheduler. */
+ * so small batches run through the dynamic book scheduler; LOB_SPLIT_BPS=n and
+ * LOB_SPLIT_MIN_MSGS=m move the bounds of the side-split build (one warp per book
+ * side, capacity <= 512, lob_process_messages only; default: at most 8 books per SM
+ * with at least 4096 messages per book -- the latency-bound RL shape; n = 0: never). */
 void lob_destroy(lob_ctx *ctx); /* frees the host handle only */
 
 /* a0: book init.  Both sides and the trade log become -1

@@ -45,6 +45,9 @@
 #ifndef LOB_SYNC_READER  // one-warp books: the __syncwarp that publishes a new order's cold
 #define LOB_SYNC_READER 1   // record runs where other lanes read records (the arg-best), not per
 #endif                      // add (C2 +1.6 %, C3 / C5 N = 100 +0.8 %, N = 256 +1.9 %; racecheck clean)
+#ifndef LOB_ADDSEL  // books of >= this many rows write an add's registers by predicated selects
+#define LOB_ADDSEL 8    // over the bounded rows instead of a compare-and-branch chain (C5 N = 256 /
+#endif              // 512 / 1024 +1.3 / +2.4 / +2.4 %, N = 2048 +-0; 4-row books: C4 -3 %, C2 -3 %)
 #ifndef LOB_TREE  // get_r as a select tree for row bounds >= LOB_TREE (0 = never; 16: C5 N = 512
 #define LOB_TREE 0  // +6 % before the {8,16} row bounds, +-0 after)
 #endif
@@ -857,7 +860,13 @@ struct Engine {
             }
         };
         // the slot's row is at most R: a compare chain instead of the jump table
-        if constexpr (R < KPL) bk.template row_r<R + 1>(slot / GT, put);
+        if constexpr (KPL >= LOB_ADDSEL) {
+            // predicated selects over rows 0..R (independent: no branch chain)
+            constexpr int RR = R < KPL ? R + 1 : KPL;
+            bk.template put_if_r<RR>(own, OWN, F_P, slot / GT, mP);
+            bk.template put_if_r<RR>(own, OWN, F_Q, slot / GT, Qa);
+            bk.template put_if_r<RR>(own, OWN, F_OID, slot / GT, mOID);
+        } else if constexpr (R < KPL) bk.template row_r<R + 1>(slot / GT, put);
         else if constexpr (KPL <= LOB_ROWR) bk.template row_r<KPL>(slot / GT, put);
         else bk.row(slot / GT, put);
         if constexpr (PRED) sts128_if0(tid, bk.rec(OWN, slot), make_int4(mOID, mTID, mTS, mTNS));  // one writer
