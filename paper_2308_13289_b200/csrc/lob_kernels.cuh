@@ -48,6 +48,12 @@
 #ifndef LOB_ADDSEL  // books of >= this many rows write an add's registers by predicated selects
 #define LOB_ADDSEL 8    // over the bounded rows instead of a compare-and-branch chain (C5 N = 256 /
 #endif              // 512 / 1024 +1.3 / +2.4 / +2.4 %, N = 2048 +-0; 4-row books: C4 -3 %, C2 -3 %)
+#ifndef LOB_FREEHINT  // multi-warp books: an add takes a known lowest empty slot without a search
+#define LOB_FREEHINT 1  // (C5 N = 1024 / 2048 +1.1 %)
+#endif
+#ifndef LOB_FREEHINT_KPL  // ... and one-warp books of at least this many rows
+#define LOB_FREEHINT_KPL 99
+#endif
 #ifndef LOB_TREE  // get_r as a select tree for row bounds >= LOB_TREE (0 = never; 16: C5 N = 512
 #define LOB_TREE 0  // +6 % before the {8,16} row bounds, +-0 after)
 #endif
@@ -399,6 +405,13 @@ struct Engine {
     static constexpr bool kSyncReader = LOB_SYNC_READER && W == 1 && !PRED;
     int bTS[2], bTNS[2];
     int hr[2];              // row high-water mark per side (see with_rows)
+    // W > 1 (LOB_FREEHINT): the add's lowest empty slot (G3) without a search where
+    // possible.  Invariant per side: every empty slot below flb is >= frm (frm = NP: none),
+    // and frm is empty -- so frm, when below NP, IS the lowest empty slot.  A searched add
+    // at s sets flb = s + 1, frm = NP; an add at frm sets flb = frm + 1, frm = NP; a removal
+    // (cancel or fill emptying slot r < flb) lowers frm to r.
+    static constexpr bool kFreeHint = LOB_FREEHINT && (W > 1 || KPL >= LOB_FREEHINT_KPL);
+    int flb[2], frm[2];
     unsigned long long bV[2];  // TL1: total quantity at the cached best price (its L1 volume,
                                // exact in 64 bits; reported saturated at INT32_MAX, G20)
     long long part_cxl;     // cancelled quantity, accumulated on the owner thread (G14)
@@ -532,6 +545,8 @@ struct Engine {
         return (KPL - 1) - (int)gmin_u((unsigned)(KPL - 1 - hl));
     }
     __device__ __forceinline__ void init_rows() {
+        flb[0] = flb[1] = 0;
+        frm[0] = frm[1] = BK::NP;
         if constexpr (ROWS) {
             hr[ASK] = top_row<ASK>();
             hr[BID] = top_row<BID>();
@@ -720,7 +735,7 @@ struct Engine {
     }
     // the cancelled order: its slot (or none, >= NP) and, on the owner thread, its Q
     template <int SD, int R>
-    __device__ __forceinline__ int cancel_find(int mP, int mOID, int &qi) {
+    __device__ __forceinline__ int cancel_find(int mP, int mOID, int &qi, int mQ, bool &emptied) {
         if constexpr (W >= LOB_CXL2_W) {
             // ONE pass, ONE group minimum: each thread's lowest exact-OID row and lowest
             // synthetic row at P (with their Q), keyed so that any exact match in the group
@@ -737,14 +752,43 @@ struct Engine {
             const unsigned key = rex < (unsigned)KPL
                                      ? rex * GT + (unsigned)tid
                                      : (rsy < (unsigned)KPL ? (unsigned)BK::NP + rsy * GT + (unsigned)tid : 2u * BK::NP);
-            const unsigned k = gmin_u(key);
-            const bool exact = k < (unsigned)BK::NP;
-            qi = exact ? qex : qsy;
-            return (int)(exact ? k : k - BK::NP);  // >= NP when neither exists
+            if constexpr (kFreeHint) {
+                // bit 0: the cancel empties the found order (min(Q, Q_i) = Q_i) --
+                // the owner's key wins the minimum, so the bit arrives uniform
+                const int qo = rex < (unsigned)KPL ? qex : qsy;
+                const unsigned k2 = gmin_u(key * 2u + (qo <= mQ ? 1u : 0u));
+                const unsigned k = k2 >> 1;
+                emptied = (k2 & 1u) != 0u;
+                const bool exact = k < (unsigned)BK::NP;
+                qi = exact ? qex : qsy;
+                return (int)(exact ? k : k - BK::NP);
+            } else {
+                const unsigned k = gmin_u(key);
+                const bool exact = k < (unsigned)BK::NP;
+                qi = exact ? qex : qsy;
+                return (int)(exact ? k : k - BK::NP);  // >= NP when neither exists
+            }
         } else {
             // exact OID first, then the synthetic fallback (G12); the scans capture
             // the Q of each thread's lowest matching row (the owner's is the found order's):
             // no select chain after the reduction (C5 N = 512 +8 %, C4 / C2 +0.3 %)
+            if constexpr (kFreeHint) {  // the same two passes, bit 0 of the key: the cancel empties it
+                const auto pass = [&](auto pred) {
+                    unsigned r = KPL;
+#pragma unroll
+                    for (int j = R - 1; j >= 0; --j)
+                        if (pred(j)) { r = (unsigned)j; qi = bk.hot(SD, F_Q, j); }
+                    const unsigned k2 = gmin_u((r * GT + (unsigned)tid) * 2u + (qi <= mQ ? 1u : 0u));
+                    emptied = (k2 & 1u) != 0u;
+                    return (int)(k2 >> 1);
+                };
+                int slot = pass([&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
+                if (!found(slot))
+                    slot = pass([&](int j) {
+                        return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) <= -9000 && bk.hot(SD, F_P, j) == mP;
+                    });
+                return slot;
+            }
             int slot = lowest_rows_q<SD, R>(qi, [&](int j) { return bk.hot(SD, F_Q, j) > 0 && bk.hot(SD, F_OID, j) == mOID; });
             if (!found(slot))
                 slot = lowest_rows_q<SD, R>(qi, [&](int j) {
@@ -756,7 +800,8 @@ struct Engine {
     template <int SD, int R>
     __device__ __forceinline__ void cancel_r(int mQ, int mP, int mOID) {
         int qi = 0;
-        const int slot = cancel_find<SD, R>(mP, mOID, qi);
+        bool emptied = false;
+        const int slot = cancel_find<SD, R>(mP, mOID, qi, mQ, emptied);
         if (!found(slot)) {                        // G15
             if constexpr (PRED) add64_if0(tid, sc + 8u * ST_UNKNOWN, 1);
             else if (tid == 0) count(ST_UNKNOWN, 1);
@@ -772,6 +817,8 @@ struct Engine {
             if (bslot[SD] >= 0) bV[SD] -= (unsigned long long)d;
         }
         if (bslot[SD] == slot) bslot[SD] = BEST_INVALID;
+        if constexpr (kFreeHint)
+            if (emptied && slot < flb[SD]) frm[SD] = min(frm[SD], slot);
     }
 
     // Limit (T=1) or market (T=4) order of side OWN.
@@ -829,7 +876,11 @@ struct Engine {
             ++ntr;                                                   // fills this call (logged = min(ntr, Tcap))
             bk.template put_if_r<R>(own, OPP, F_Q, sj, Qs2);         // filled order removed (G10)
             if constexpr (TL1) bV[OPP] -= (unsigned long long)q;
-            if (Qs2 == 0) bslot[OPP] = BEST_INVALID;
+            if (Qs2 == 0) {
+                bslot[OPP] = BEST_INVALID;
+                if constexpr (kFreeHint)
+                    if (s < flb[OPP]) frm[OPP] = min(frm[OPP], s);
+            }
         }
         return Qa;
     }
@@ -840,16 +891,22 @@ struct Engine {
     // exists -- ONE compare against N after the reduction decides saturation.
     template <int OWN, int R>
     __device__ __forceinline__ void add_r(int Qa, int mP, int mOID, int mTID, int mTS, int mTNS) {
-        unsigned r = KPL;
-        if constexpr (R < KPL) r = (unsigned)R;
+        int slot;
+        if (kFreeHint && frm[OWN] < BK::NP) {
+            slot = frm[OWN];                                         // the lowest empty slot, known
+        } else {
+            unsigned r = KPL;
+            if constexpr (R < KPL) r = (unsigned)R;
 #pragma unroll
-        for (int j = R - 1; j >= 0; --j)
-            if (bk.hot(OWN, F_Q, j) <= 0) r = (unsigned)j;
-        const int slot = (int)gmin_u(r * GT + (unsigned)tid);
-        if (slot >= p.N) {                                           // side saturated (G6)
-            if (tid == 0) { count(ST_ADD_OVF, 1); count(ST_OVF_QTY, Qa); }
-            return;
+            for (int j = R - 1; j >= 0; --j)
+                if (bk.hot(OWN, F_Q, j) <= 0) r = (unsigned)j;
+            slot = (int)gmin_u(r * GT + (unsigned)tid);
+            if (slot >= p.N) {                                       // side saturated (G6)
+                if (tid == 0) { count(ST_ADD_OVF, 1); count(ST_OVF_QTY, Qa); }
+                return;
+            }
         }
+        if constexpr (kFreeHint) { flb[OWN] = slot + 1; frm[OWN] = BK::NP; }
         const bool own = tid == (slot & (GT - 1));
         if constexpr (ROWS) hr[OWN] = max(hr[OWN], slot / GT);
         const auto put = [&](auto J) {                               // G27

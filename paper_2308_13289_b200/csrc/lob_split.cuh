@@ -151,6 +151,8 @@ __device__ __forceinline__ void split_side(const Params &p, unsigned char *regio
     }
     e.hr[X] = e.template top_row<X>();
     e.hr[Y] = KPL - 1;
+    e.flb[0] = e.flb[1] = 0;
+    e.frm[0] = e.frm[1] = NP;
     e.bslot[X] = e.bslot[Y] = BEST_INVALID;
     e.bP[X] = e.bP[Y] = 0;
     e.bV[0] = e.bV[1] = 0;
