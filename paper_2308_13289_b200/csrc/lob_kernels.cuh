@@ -48,6 +48,9 @@
 #ifndef LOB_ADDSEL  // books of >= this many rows write an add's registers by predicated selects
 #define LOB_ADDSEL 8    // over the bounded rows instead of a compare-and-branch chain (C5 N = 256 /
 #endif              // 512 / 1024 +1.3 / +2.4 / +2.4 %, N = 2048 +-0; 4-row books: C4 -3 %, C2 -3 %)
+#ifndef LOB_X4  // 4-warp books: cross-warp reductions finish with one broadcast load
+#define LOB_X4 1
+#endif
 #ifndef LOB_FREEHINT  // multi-warp books: an add takes a known lowest empty slot without a search
 #define LOB_FREEHINT 1  // (C5 N = 1024 / 2048 +1.1 %)
 #endif
@@ -440,20 +443,40 @@ struct Engine {
         xph ^= 1;  // the other buffer next time: no write-after-read race with one barrier
         return v;
     }
+    // W = 4 (LOB_X4): the four warp partials side by side, read by every lane with ONE
+    // 16-byte broadcast load and combined in registers (no second warp reduction)
+    static constexpr bool kX4 = (W == 4) && LOB_X4;
+    __device__ __forceinline__ int4 exchange4(unsigned r) {
+        const uint32_t base = xbase();
+        if ((tid & 31) == 0) sts32(base + 4u * (tid >> 5), (int)r);
+        __syncthreads();
+        const int4 v = lds128(base);
+        xph ^= 1;
+        return v;
+    }
     __device__ __forceinline__ unsigned gmin_u(unsigned x) {
         const unsigned r = __reduce_min_sync(FULL, x);
         if constexpr (W == 1) return r;
-        else return __reduce_min_sync(FULL, exchange(r, 0xffffffffu));
+        else if constexpr (kX4) {
+            const int4 v = exchange4(r);
+            return min(min((unsigned)v.x, (unsigned)v.y), min((unsigned)v.z, (unsigned)v.w));
+        } else return __reduce_min_sync(FULL, exchange(r, 0xffffffffu));
     }
     __device__ __forceinline__ int gmin_i(int x) {
         const int r = __reduce_min_sync(FULL, x);
         if constexpr (W == 1) return r;
-        else return __reduce_min_sync(FULL, (int)exchange((unsigned)r, (unsigned)INT_MAX));
+        else if constexpr (kX4) {
+            const int4 v = exchange4((unsigned)r);
+            return min(min(v.x, v.y), min(v.z, v.w));
+        } else return __reduce_min_sync(FULL, (int)exchange((unsigned)r, (unsigned)INT_MAX));
     }
     __device__ __forceinline__ unsigned gadd(unsigned x) {
         const unsigned r = __reduce_add_sync(FULL, x);
         if constexpr (W == 1) return r;
-        else return __reduce_add_sync(FULL, exchange(r, 0u));
+        else if constexpr (kX4) {
+            const int4 v = exchange4(r);
+            return ((unsigned)v.x + (unsigned)v.y) + ((unsigned)v.z + (unsigned)v.w);
+        } else return __reduce_add_sync(FULL, exchange(r, 0u));
     }
     // exact group sum of per-thread partials < 2^35 (sums of up to 16 int32 quantities):
     // two 32-bit reductions of the high and low 16-bit halves (each total < 2^27)
