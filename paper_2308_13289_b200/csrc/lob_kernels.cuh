@@ -454,6 +454,16 @@ struct Engine {
         xph ^= 1;
         return v;
     }
+    // two warp-reduced values per warp: warp k's pair lands in (a.x, a.y) / (a.z, a.w) /
+    // (b.x, b.y) / (b.z, b.w) for k = 0..3
+    __device__ __forceinline__ void exchange_pair4(unsigned r0, unsigned r1, int4 &a, int4 &b) {
+        const uint32_t base = xbase();
+        if ((tid & 31) == 0) sts64(base + 8u * (tid >> 5), (long long)(((unsigned long long)r1 << 32) | r0));
+        __syncthreads();
+        a = lds128(base);
+        b = lds128(base + 16u);
+        xph ^= 1;
+    }
     __device__ __forceinline__ unsigned gmin_u(unsigned x) {
         const unsigned r = __reduce_min_sync(FULL, x);
         if constexpr (W == 1) return r;
@@ -1017,6 +1027,32 @@ struct Engine {
             const bool occ = bk.hot(SD, F_Q, j) > 0;
             key[j] = occ ? ((SD == ASK) ? (unsigned)(p - 1) : (unsigned)(INT_MAX - p)) : 0xffffffffu;
             if (occ) hl = j;
+        }
+        if constexpr (kX4) {
+            // 4-warp books: level k's volume and level k+1's price travel in ONE exchange
+            // (the next minimum needs only this thread's keys once level k is retired), and
+            // the row bound rides with level 0's price: L + 1 barriers instead of 2 L + 1
+            unsigned lk = key[0];
+#pragma unroll
+            for (int j = 1; j < R; ++j) lk = min(lk, key[j]);
+            int4 a, b;
+            exchange_pair4(__reduce_min_sync(FULL, (unsigned)(KPL - 1 - hl)), __reduce_min_sync(FULL, lk), a, b);
+            if constexpr (ROWS) hr[SD] = (KPL - 1) - (int)min(min((unsigned)a.x, (unsigned)a.z), min((unsigned)b.x, (unsigned)b.z));
+            unsigned m = min(min((unsigned)a.y, (unsigned)a.w), min((unsigned)b.y, (unsigned)b.w));
+            for (int k = 0; k < L; ++k) {
+                if (m == 0xffffffffu) break;
+                unsigned lq = 0, nk = 0xffffffffu;
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    if (key[j] == m) { lq += (unsigned)bk.hot(SD, F_Q, j); key[j] = 0xffffffffu; }
+                    nk = min(nk, key[j]);
+                }
+                exchange_pair4(__reduce_add_sync(FULL, lq), __reduce_min_sync(FULL, nk), a, b);
+                const unsigned qs = ((unsigned)a.x + (unsigned)a.z) + ((unsigned)b.x + (unsigned)b.z);
+                if (tid == k) { outp = (SD == ASK) ? (int)(m + 1u) : (int)(INT_MAX - (int)m); outq = (int)qs; }
+                m = min(min((unsigned)a.y, (unsigned)a.w), min((unsigned)b.y, (unsigned)b.w));
+            }
+            return;
         }
         if constexpr (ROWS) hr[SD] = (KPL - 1) - (int)gmin_u((unsigned)(KPL - 1 - hl));  // exact row bound again
         for (int k = 0; k < L; ++k) {
