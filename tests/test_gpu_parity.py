@@ -121,6 +121,18 @@ def test_side_split_build(monkeypatch, split, profile, N, Tcap, calls):
     assert_outputs_equal(g, o, what=f"split={split} {profile} N={N} Tcap={Tcap} calls={calls}")
 
 
+@pytest.mark.parametrize("M,steps,L", [(37, 9, 10), (1, 70, 3), (200, 3, 32), (33, 4, 1)])
+def test_side_split_ragged_steps(monkeypatch, M, steps, L):
+    # step ends in the middle of a staging chunk, one-message steps, steps spanning several
+    # chunks, a ragged last chunk: the per-side L2 snapshots and the chunk-granular
+    # progress / window logic of the side-split build
+    monkeypatch.setenv("LOB_SPLIT_BPS", "100000")
+    monkeypatch.setenv("LOB_SPLIT_MIN_MSGS", "0")
+    cfg = lobgen.Config("sr", 257, 100, steps, M, 20, 512, L, "heavy_market", 7 * M + steps)
+    g, o = _both(cfg)
+    assert_outputs_equal(g, o, what=f"split ragged M={M} steps={steps} L={L}")
+
+
 @pytest.mark.parametrize("L,Tcap", [(1, 0), (32, 3), (10, 1)])
 def test_levels_and_tiny_trade_log(L, Tcap):
     cfg = lobgen.Config("p", 200, 100, 5, 50, 40, Tcap, L, "heavy_market", 5)
