@@ -56,7 +56,8 @@ def test_configs_subset(name, n):
 @pytest.mark.parametrize("profile,N", [("ties", 100), ("overflow", 16), ("synthetic", 100),
                                        ("garbage", 100), ("heavy_market", 64), ("lobster", 1),
                                        ("lobster", 33), ("lobster", 97), ("overflow", 130),
-                                       ("garbage", 300), ("ties", 1024)])
+                                       ("garbage", 300), ("ties", 1024), ("garbage", 1024),
+                                       ("garbage", 2000), ("synthetic", 1500)])
 def test_profiles(profile, N):
     cfg = lobgen.Config("p", 333, N, 7, 37, min(N, 12), 50, 10, profile, 21 + N)
     g, o = _both(cfg)
