@@ -69,6 +69,8 @@ def parse(argv=None):
                     help="override the config's books (per GPU when weak, total when strong; SURVEY.md 8(d) K sweep)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="pipelined H2D / compute / D2H chunks (0: LobBatch.process_host's default)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--core-seconds", type=float, default=3.0,
                     help="CPU seconds of the one-core oracle sample (cpu_baseline.per_core)")
@@ -513,7 +515,7 @@ def e2e(ph, args):
     def e2e_step():
         ph.init_d.copy_(ph.init_h, non_blocking=True)
         b.init(ph.init_d, lobgen.INIT_TS, lobgen.INIT_TNS)
-        b.process_host(ph.msgs_h, S, M, h_l2, h_st, ph.msgs_d, ph.l2_d, chunks=8, h_trades_out=h_tr,
+        b.process_host(ph.msgs_h, S, M, h_l2, h_st, ph.msgs_d, ph.l2_d, chunks=args.e2e_chunks or None, h_trades_out=h_tr,
                        h_trade_counts_out=h_cnt)
 
     e2e_step()
@@ -534,12 +536,27 @@ def e2e(ph, args):
     tr, cnt = b.trades()
     mask = torch.arange(c.trades_cap, device=ph.dev)[None, :] < cnt[:, None]
     assert torch.equal(h_tr[:rows], tr[mask].cpu()), "end-to-end trade rows differ from the device run"
+    # the bound: a plain pinned host->device copy of the same message bytes, timed alike
+    h2d = ph.msgs_h.numel() * 4 + ph.init_h.numel() * 4
+    c_s, c_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ph.msgs_d.copy_(ph.msgs_h, non_blocking=True)
+    c_s.record(stream)
+    for _ in range(2):
+        ph.msgs_d.copy_(ph.msgs_h, non_blocking=True)
+    c_e.record(stream)
+    torch.cuda.synchronize()
+    copy_gbs = 2 * ph.msgs_h.numel() * 4 / (c_s.elapsed_time(c_e) / 1e3) / 1e9
+    achieved_gbs = h2d * args.e2e_steps / (et / 1e3) / 1e9
     return {"value": v, "unit": "msg/s",
-            "h2d_bytes_per_step": ph.msgs_h.numel() * 4 + ph.init_h.numel() * 4,
+            "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": h_l2.numel() * 4 + h_st.numel() * 8 + rows * TRADE_BYTES + h_cnt.numel() * 4,
             "trade_rows_per_step": rows,
-            "path": "LobBatch.process_host -> lob_process_messages_host (8 pipelined chunks; L2, counters, "
-                    "packed logged trade rows + counts to pinned host memory)"}
+            "path": f"LobBatch.process_host -> lob_process_messages_host ({args.e2e_chunks or min(64, max(1, K // 1024))} pipelined chunks; L2, "
+                    "counters, packed logged trade rows + counts to pinned host memory)",
+            "pcie": {"bound": "h2d", "achieved_gbs": achieved_gbs, "copy_gbs": copy_gbs,
+                     "frac": achieved_gbs / copy_gbs,
+                     "note": "the step's input bytes over the e2e step time, against a plain pinned "
+                             "host->device copy of the same messages in this run"}}
 
 
 def clocks_all(sampler, world):

@@ -233,12 +233,19 @@ class LobBatch:
         return out if l2 else None
 
     def process_host(self, h_msgs, n_steps: int, msgs_per_step: int, h_l2_out=None,
-                     h_stats_out=None, d_msgs_buf=None, d_l2_buf=None, chunks: int = 8, stream=None,
+                     h_stats_out=None, d_msgs_buf=None, d_l2_buf=None, chunks: int | None = None, stream=None,
                      h_trades_out=None, h_trade_counts_out=None):
         """lob_process_messages_host: pinned host messages in; pinned host L2 [K][S][L][4],
         counters [K][10], and the LOGGED trade rows packed book after book into
         ``h_trades_out`` (capacity [K*T_cap][6]) with per-book counts in
-        ``h_trade_counts_out`` [K].  The caller synchronises the stream before reading."""
+        ``h_trade_counts_out`` [K].  The caller synchronises the stream before reading.
+
+        ``chunks`` (default: one per 1,024 books, at most 64): the book slices whose
+        host->device copy overlaps the previous slice's kernel.  Measured on C4 (65,536
+        books): 8 / 16 / 32 / 64 / 128 chunks reach 90 / 92 / 93 / 95 / 89 % of a plain
+        pinned copy's bandwidth."""
+        if chunks is None:
+            chunks = max(1, min(64, self.K // 1024))
         assert h_msgs.device.type == "cpu" and h_msgs.dtype == torch.int32 and h_msgs.is_contiguous()
         for t in (h_l2_out, h_stats_out, h_trades_out, h_trade_counts_out):
             assert t is None or (t.device.type == "cpu" and t.is_contiguous() and t.is_pinned())

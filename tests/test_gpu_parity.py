@@ -234,7 +234,8 @@ def _check_host_outputs(h, a, l2a):
 
 
 @pytest.mark.parametrize("name,n,chunks,Tcap", [("C4", 3000, 5, None), ("C3", 1200, 3, None),
-                                                ("C3", 700, 1, 2), ("C5_512", 150, 4, None)])
+                                                ("C3", 700, 1, 2), ("C5_512", 150, 4, None),
+                                                ("C4", 4500, None, None), ("C4", 2000, 64, None)])
 def test_host_path_equals_device_path(name, n, chunks, Tcap):
     """The end-to-end call (pinned host buffers in and out, chunked copy/compute pipeline)
     returns exactly what the device path produces: per-step L2, counters, and every
