@@ -60,6 +60,18 @@
 #ifndef LOB_TREE  // get_r as a select tree for row bounds >= LOB_TREE (0 = never; 16: C5 N = 512
 #define LOB_TREE 0  // +6 % before the {8,16} row bounds, +-0 after)
 #endif
+#ifndef LOB_R16W  // 16-row multi-warp books: lower row bound (0: the one-warp {8, 16}); {6, 8, 16}:
+#define LOB_R16W 6  // C5 N = 2048 +10 % (682 resting orders fill 5.3 rows of 128 slots)
+#endif
+#ifndef LOB_R8W  // 8-row multi-warp books: an extra lower row bound (0: none); {3, 4, 8}:
+#define LOB_R8W 3  // C5 N = 1024 +7 % (128 slots per row: 341 resting orders fill 2.7 rows)
+#endif
+#ifndef LOB_R16W8  // ... with a middle bound of 8 rows ({6, 16} measured the same)
+#define LOB_R16W8 1
+#endif
+#ifndef LOB_R16LO  // 16-row one-warp books: lower row bound (7: C5 N = 512 +0.8 %, 6: -33 %)
+#define LOB_R16LO 8
+#endif
 #ifndef LOB_R8    // row bounds of 8-row books: 0 = {2,4,8}, 1 = {4,8} (C5 N = 256 +13 %, N = 1024 +4 %),
 #define LOB_R8 1  // 2 = {2,8} (-10 %, -16 %)
 #endif
@@ -542,8 +554,14 @@ struct Engine {
 #endif
         } else if constexpr (KPL <= 8) {
 #if LOB_R8 == 1
-            if (h < 4) f(IC<4>{});
-            else f(IC<KPL>{});
+            if constexpr (W > 1 && LOB_R8W > 0) {  // multi-warp books: {LOB_R8W, 4, 8}
+                if (h < LOB_R8W) f(IC<LOB_R8W>{});
+                else if (h < 4) f(IC<4>{});
+                else f(IC<KPL>{});
+            } else {
+                if (h < 4) f(IC<4>{});
+                else f(IC<KPL>{});
+            }
 #elif LOB_R8 == 2
             if (h < 2) f(IC<2>{});
             else f(IC<KPL>{});
@@ -563,8 +581,16 @@ struct Engine {
             else if (h < 8) f(IC<8>{});
             else f(IC<KPL>{});
 #else  // {8, 16}: C5 N = 512 +24 %, N = 2048 +5 % over {4, 8, 16} (fewer code copies)
-            if (h < 8) f(IC<8>{});
-            else f(IC<KPL>{});
+            if constexpr (W > 1 && LOB_R16W > 0) {  // multi-warp books: {LOB_R16W, (8,) 16}
+                if (h < LOB_R16W) f(IC<LOB_R16W>{});
+#if LOB_R16W8
+                else if (h < 8) f(IC<8>{});
+#endif
+                else f(IC<KPL>{});
+            } else {
+                if (h < LOB_R16LO) f(IC<LOB_R16LO>{});
+                else f(IC<KPL>{});
+            }
 #endif
         }
     }
