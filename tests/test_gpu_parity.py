@@ -337,7 +337,7 @@ def test_env_rejects_agent_oid_base_zero():
         env.reset(34200, 0)
 
 
-@pytest.mark.parametrize("name", ["C4", "C3", "C5_32", "C5_100", "C5_512", "C5_2048"])
+@pytest.mark.parametrize("name", ["C4", "C3", "C2", "C5_32", "C5_100", "C5_256", "C5_512", "C5_1024", "C5_2048"])
 def test_full_size_sampled_books(name):
     """Every BASELINE.json config at its full size (C4: 65,536 books, the launch
     configuration bench.py times; C3: 16,384; C5: 4,096 at each capacity), sampled
