@@ -1302,8 +1302,8 @@ constexpr int step_smem_bytes() {
 #ifndef MINB4
 #define MINB4 7
 #endif
-#ifndef MINB16
-#define MINB16 3
+#ifndef MINB16  // 16-row one-warp books (MODE 0): register budget of 4 CTAs/SM (128 registers;
+#define MINB16 4   // shared memory still allows 3): C5 N = 512 +1 % over the 168-register build
 #endif
 #ifndef MINB8W  // 8-row 4-warp books: CTAs (books) per SM the registers are sized for
 #define MINB8W 5  // (5: 96 registers, C5 N = 1024 +8 % over 4; 6: +4 %; the L1 / env builds keep 4)
@@ -1321,7 +1321,7 @@ constexpr int step_smem_bytes() {
 // resident CTAs per SM the register budget is sized for
 template <int KPL, int W, int MODE>
 constexpr int step_min_blocks() {
-    return MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? (KPL > 8 ? MINB16 : MINB8) : (KPL > 8 ? 12 / W : (MODE == 0 ? MINB8W : 16 / W)))));
+    return MODE == 3 ? 8 : (KPL <= 2 ? 7 : (KPL <= 4 ? MINB4 : (W == 1 ? (KPL > 8 ? (MODE == 0 ? MINB16 : 3) : MINB8) : (KPL > 8 ? 12 / W : (MODE == 0 ? MINB8W : 16 / W)))));
 }
 template <int KPL, int W, int G, int MODE>
 __global__ void __launch_bounds__(32 * W * G, step_min_blocks<KPL, W, MODE>())

@@ -94,7 +94,7 @@ __device__ __forceinline__ unsigned session_step_sync(const SessionParams &sp, u
 // get 96 registers (5 CTAs/SM: up to 2,960 resident books; no spills -- at 72 registers
 // the per-step state spilled 40 bytes); larger books the lob_step budget.
 template <int KPL, int W, int G>
-__global__ void __launch_bounds__(32 * W * G, (KPL <= 4 ? 5 : (W == 1 ? (KPL > 8 ? MINB16 : 3) : (KPL > 8 ? 12 / W : 16 / W))))
+__global__ void __launch_bounds__(32 * W * G, (KPL <= 4 ? 5 : (W == 1 ? 3 : (KPL > 8 ? 12 / W : 16 / W))))
     lob_session(const Params p, const EnvParams ep, const SessionParams sp) {
     using BK = RegBook<KPL, W>;
     extern __shared__ __align__(128) unsigned char dyn[];
